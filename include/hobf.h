@@ -1,0 +1,129 @@
+/*
+ * hobf.h -- C ABI of the B200-native HOBFLOPS hot path (arXiv 2007.06563):
+ * bitslice-parallel custom-precision floating-point multiply-accumulate inside
+ * a CNN convolution, on sm_100a.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (the reference text).
+ *
+ * DATA FORMATS
+ *   Word (one element, low NBITS bits of a uint32): FloPoCo encoding
+ *     [exc:2 | sign:1 | exp:wE | frac:wF], MSB to LSB; exc 00 zero, 01 normal,
+ *     10 inf, 11 NaN; significand 1.frac, bias 2^(wE-1)-1, every
+ *     exponent code normal, no subnormals.  NBITS = 2+1+wE+wF.
+ *   Planes (bitslice layout, Fig. 4a): a [rows][C] array of words
+ *     is stored as uint32 planes[rows][ceil(C/32)][NP], NP = hobf_nplanes(NBITS)
+ *     = roundup(NBITS, 4); bit l of plane word (r, g, j) is field bit j of
+ *     element (r, 32g + l).  Padding lanes and planes are zero (+0).
+ *   Conv tensors: activations NHWC (rows = n*h*w, C = cin); weights
+ *     [kh][kw][cin][cout] (rows = kh*kw*cin, C = cout); outputs NHWC
+ *     (rows = n*ho*wo, C = cout) in the MAC output format F(wE, hobf_out_wf(f)).
+ *
+ * MAC SEMANTICS
+ *   single class: product and accumulator fraction width wF+1; RNE or RTZ in
+ *   both the multiplier and the adder; overflow -> inf, underflow -> zero with
+ *   sign, exact cancellation -> +0; each output is acc = +0 then
+ *   acc = add(acc, mul(x, w)) serially over (c, kh, kw), c outermost, with
+ *   zero padding taps included; optional ReLU.
+ *
+ * CONVENTIONS
+ *   - The caller owns every buffer; device pointers must be 16-byte aligned.
+ *     The library keeps no device allocation and no mutable global state.
+ *   - Argument checks are synchronous and return HOBF_EINVAL (null pointer,
+ *     negative size, misaligned pointer, format out of range) / HOBF_ESHAPE
+ *     (inconsistent shapes) / HOBF_EUNSUPPORTED (no generated kernel for the
+ *     format) before anything is launched.  Work is enqueued asynchronously on
+ *     `stream` (a cudaStream_t; NULL = legacy default stream); a launch failure
+ *     returns HOBF_ECUDA.  Nothing aborts or throws across the ABI.
+ *   - Words are not validated on the device: pack is total (masks to NBITS and
+ *     canonicalises: exc != 01 -> exp = frac = 0, NaN sign 0).
+ */
+#ifndef HOBF_H
+#define HOBF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HOBF_OK = 0,
+  HOBF_EINVAL = 1,
+  HOBF_ESHAPE = 2,
+  HOBF_EUNSUPPORTED = 3,
+  HOBF_ECUDA = 4
+} hobf_status;
+
+typedef enum { HOBF_RNE = 0, HOBF_RTZ = 1 } hobf_round;
+
+/* Input format + MAC mode.  extended: 0 = single class (wF+1), 1 = extended
+ * (2wF+1; not yet implemented on the GPU -> HOBF_EUNSUPPORTED). */
+typedef struct {
+  int32_t we, wf, round, extended;
+} hobf_fmt;
+
+typedef void* hobf_stream; /* cudaStream_t */
+
+/* NINBITS = 2+1+we+wf. */
+int32_t hobf_nbits(int32_t we, int32_t wf);
+/* Fraction width of the MAC output: wf+1 (single) or 2wf+1 (extended) (Table 4). */
+int32_t hobf_out_wf(hobf_fmt f);
+/* Words per 32-lane plane group: roundup(nbits, 4). */
+int32_t hobf_nplanes(int32_t nbits);
+/* rows * ceil(c/32) * hobf_nplanes(nbits): size of a plane buffer in uint32 words. */
+int64_t hobf_planes_words(int64_t rows, int64_t c, int32_t nbits);
+
+/* Bitslice transform: words[rows][c] (F(we,wf) words, device) ->
+ * planes (device).  Masks to NBITS and canonicalises. */
+hobf_status hobf_pack(int32_t we, int32_t wf, const uint32_t* d_words, int64_t rows, int64_t c,
+                      uint32_t* d_planes, hobf_stream stream);
+
+/* Quantise float32 values x[rows][c] (device) into F(we, wf) with `round`
+ * (RNE/RTZ at the value's own binade; NaN -> NaN, +-inf -> +-inf, +-0 -> +-0,
+ * overflow -> inf, underflow -> zero with sign)
+ * and pack into planes (device), one kernel. */
+hobf_status hobf_quantize_pack(int32_t we, int32_t wf, int32_t round, const float* d_x, int64_t rows,
+                               int64_t c, uint32_t* d_planes, hobf_stream stream);
+
+/* Inverse transform: planes -> words[rows][c] (device). */
+hobf_status hobf_unpack(int32_t we, int32_t wf, const uint32_t* d_planes, int64_t rows, int64_t c,
+                        uint32_t* d_words, hobf_stream stream);
+
+/* planes -> float32 values (exact for we <= 7; "transformed ... to floats"). */
+hobf_status hobf_unpack_f32(int32_t we, int32_t wf, const uint32_t* d_planes, int64_t rows, int64_t c,
+                            float* d_x, hobf_stream stream);
+
+/* HOBFLOPS convolution (Fig. 5): x planes (format f.we/f.wf),
+ * weight planes (same format), output planes in F(f.we, hobf_out_wf(f)).
+ * ho = (h + 2 pad - kh)/stride + 1, wo likewise; both must be >= 1. */
+hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
+                        const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
+                        int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream);
+
+/* Lane-wise MAC on plane groups: acc = add(acc, mul(a, b)).  acc: [n_groups][NP(NOUT)],
+ * a, b: [n_groups][NP(NIN)] (device).  One step of the conv reduction. */
+hobf_status hobf_mac_planes(hobf_fmt f, uint32_t* d_acc, const uint32_t* d_a, const uint32_t* d_b,
+                            int64_t n_groups, hobf_stream stream);
+
+/* Gate counts of the generated circuits (lop3 per 32 lanes; P:249 analogue):
+ * mac = multiplier and adder mapped jointly (the conv inner loop body). Any
+ * output pointer may be NULL. */
+hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add, int32_t* relu);
+
+/* LOP3 issue-rate microbenchmark (roofline denominator): launches `blocks` x
+ * `threads` threads, each issuing `iters` x 128 dependent-free lop3 ops;
+ * *lop3_per_launch receives the thread-op count.  d_sink: >= 4 KiB device. */
+hobf_status hobf_lop3_peak(int32_t blocks, int32_t threads, int32_t iters, uint32_t* d_sink,
+                           hobf_stream stream, int64_t* lop3_per_launch);
+
+/* Number of kernel launches the previous successful call on this thread enqueued. */
+int32_t hobf_last_launch_count(void);
+
+const char* hobf_status_str(hobf_status s);
+const char* hobf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HOBF_H */

@@ -1,0 +1,331 @@
+// hobf_capi.cu -- the C ABI (include/hobf.h) and the format-generic kernels:
+// bitslice pack / quantise+pack / unpack / unpack-to-float32, and the LOP3
+// issue-rate microbenchmark.  Per-format conv / MAC kernels live in the
+// generated translation units (csrc/gen/hobf_fmt_*.cu) and are reached
+// through the dispatch table below.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/hobf.h"
+#include "hobf_internal.h"
+
+using hobf::ConvArgs;
+using hobf::FormatEntry;
+
+#define HOBF_DECLARE(TAG)                                                                    \
+  cudaError_t hobf_launch_conv_##TAG(const hobf::ConvArgs& a, cudaStream_t s);               \
+  cudaError_t hobf_launch_mac_##TAG(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n, \
+                                    cudaStream_t s);
+#define HOBF_ENTRY(TAG, WE, WF, RND, GM, GMUL, GADD, GRELU) \
+  {WE, WF, RND, GM, GMUL, GADD, GRELU, hobf_launch_conv_##TAG, hobf_launch_mac_##TAG},
+#include "gen/hobf_table.inc"
+
+static const FormatEntry kFormats[] = {HOBF_TABLE_ENTRIES};
+static const int kNumFormats = (int)(sizeof(kFormats) / sizeof(kFormats[0]));
+
+static thread_local int32_t g_last_launches = 0;
+
+static const FormatEntry* find_format(int we, int wf, int rnd) {
+  for (int i = 0; i < kNumFormats; i++)
+    if (kFormats[i].we == we && kFormats[i].wf == wf && kFormats[i].rnd == rnd) return &kFormats[i];
+  return nullptr;
+}
+
+static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+static inline bool fmt_ok(int we, int wf) { return we >= 2 && we <= 8 && wf >= 1 && 3 + we + wf <= 32; }
+
+// ----------------------------------------------------------------------------- device helpers
+
+// Canonical form: mask to NBITS; exc != 01 -> exp = frac = 0; NaN -> sign 0.
+__device__ __forceinline__ uint32_t canon_word(uint32_t v, int we, int wf) {
+  const int nb = 3 + we + wf;
+  v &= (nb >= 32) ? 0xffffffffu : ((1u << nb) - 1u);
+  const uint32_t exc = (v >> (wf + we + 1)) & 3u;
+  if (exc != 1u) v &= ~((1u << (wf + we)) - 1u);
+  if (exc == 3u) v &= ~(1u << (wf + we));
+  return v;
+}
+
+// float32 -> F(we, wf): exact value M*2^e of the float,
+// rounded at its own binade (RNE ties-to-even or RTZ), then overflow -> inf,
+// underflow (biased exponent < 0) -> zero keeping the sign (L5/L6).
+__device__ __forceinline__ uint32_t encode_f32(float f, int we, int wf, int rnd) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t sign = u >> 31;
+  const int ex = (int)((u >> 23) & 0xFFu);
+  const uint32_t man = u & 0x7FFFFFu;
+  const int top = wf + we + 1;
+  if (ex == 0xFF) return man ? (3u << top) : ((2u << top) | (sign << (wf + we)));
+  if (ex == 0 && man == 0) return sign << (wf + we);
+  uint32_t M;
+  int e;
+  if (ex == 0) { M = man; e = -149; } else { M = man | 0x800000u; e = ex - 150; }
+  const int k = 31 - __clz(M);  // M = 1.xxx * 2^k
+  const int sh = k - wf;
+  uint32_t q;
+  if (sh <= 0) {
+    q = M << (-sh);
+  } else {
+    q = M >> sh;
+    const uint32_t rem = M & ((1u << sh) - 1u);
+    const uint32_t half = 1u << (sh - 1);
+    if (rnd == 0 && (rem > half || (rem == half && (q & 1u)))) q += 1u;
+  }
+  int E = e + k + ((1 << (we - 1)) - 1);
+  if (q == (2u << wf)) { q >>= 1; E += 1; }
+  if (E > (1 << we) - 1) return (2u << top) | (sign << (wf + we));
+  if (E < 0) return sign << (wf + we);
+  return (1u << top) | (sign << (wf + we)) | ((uint32_t)E << wf) | (q - (1u << wf));
+}
+
+// F(we, wf) word -> float32 (exact for we <= 7, wf <= 23).
+__device__ __forceinline__ float decode_f32(uint32_t v, int we, int wf) {
+  const uint32_t exc = (v >> (wf + we + 1)) & 3u;
+  const uint32_t sign = (v >> (wf + we)) & 1u;
+  if (exc == 0u) return __uint_as_float(sign << 31);
+  if (exc == 2u) return __uint_as_float((sign << 31) | 0x7F800000u);
+  if (exc == 3u) return __uint_as_float(0x7FC00000u);
+  const int E = (int)((v >> wf) & ((1u << we) - 1u)) - ((1 << (we - 1)) - 1);
+  const uint32_t frac = v & ((1u << wf) - 1u);
+  return __uint_as_float((sign << 31) | ((uint32_t)(E + 127) << 23) | (frac << (23 - wf)));
+}
+
+// ----------------------------------------------------------------------------- pack / unpack
+// One warp per (row, 32-lane group): lane l holds element 32g+l; plane j is
+// the warp ballot of bit j.  Coalesced 128-byte word reads and
+// 4*NP-byte plane writes.
+
+template <bool FROM_F32>
+__global__ void __launch_bounds__(256) pack_kernel(const void* __restrict__ src, int64_t rows, int64_t C, int we,
+                                                   int wf, int rnd, int np, uint32_t* __restrict__ planes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t G = (C + 31) >> 5;
+  const int64_t items = rows * G;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    const int64_t r = it / G;
+    const int64_t c = (it - r * G) * 32 + lane;
+    uint32_t v = 0u;
+    if (c < C) {
+      if (FROM_F32)
+        v = encode_f32(__ldg(reinterpret_cast<const float*>(src) + r * C + c), we, wf, rnd);
+      else
+        v = canon_word(__ldg(reinterpret_cast<const uint32_t*>(src) + r * C + c), we, wf);
+    }
+    uint32_t mine = 0u;
+    for (int j = 0; j < np; j++) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (v >> j) & 1u);
+      if (lane == j) mine = bal;
+    }
+    if (lane < np) planes[it * np + lane] = mine;
+  }
+}
+
+template <bool TO_F32>
+__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict__ planes, int64_t rows, int64_t C,
+                                                     int we, int wf, int np, void* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t G = (C + 31) >> 5;
+  const int64_t items = rows * G;
+  const int nb = 3 + we + wf;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    const uint32_t mine = lane < np ? __ldg(planes + it * np + lane) : 0u;
+    uint32_t v = 0u;
+    for (int j = 0; j < nb; j++) {
+      const uint32_t pj = __shfl_sync(0xffffffffu, mine, j);
+      v |= ((pj >> lane) & 1u) << j;
+    }
+    const int64_t r = it / G;
+    const int64_t c = (it - r * G) * 32 + lane;
+    if (c < C) {
+      if (TO_F32)
+        reinterpret_cast<float*>(dst)[r * C + c] = decode_f32(v, we, wf);
+      else
+        reinterpret_cast<uint32_t*>(dst)[r * C + c] = v;
+    }
+  }
+}
+
+static unsigned warp_grid(int64_t items) {
+  int64_t blocks = (items + 7) / 8;  // 8 warps per 256-thread block
+  const int64_t cap = 148 * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (unsigned)blocks;
+}
+
+// ----------------------------------------------------------------------------- lop3 peak
+__global__ void lop3_peak_kernel(uint32_t* sink, uint32_t seed, int iters) {
+  uint32_t v[8];
+  const uint32_t a = seed ^ threadIdx.x, b = seed * 7u + blockIdx.x;
+#pragma unroll
+  for (int i = 0; i < 8; i++) v[i] = a + i * 0x9E3779B9u;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        uint32_t r;
+        if ((k + i) & 1)
+          asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(v[i]), "r"(a), "r"(b));
+        else
+          asm volatile("lop3.b32 %0, %1, %2, %3, 0xE8;" : "=r"(r) : "r"(v[i]), "r"(b), "r"(a));
+        v[i] = r;
+      }
+    }
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) x ^= v[i];
+  if (x == 0x12345678u) sink[threadIdx.x & 1023] = x;
+}
+
+// ----------------------------------------------------------------------------- C ABI
+extern "C" {
+
+int32_t hobf_nbits(int32_t we, int32_t wf) { return 3 + we + wf; }
+
+int32_t hobf_out_wf(hobf_fmt f) { return f.extended ? 2 * f.wf + 1 : f.wf + 1; }
+
+int32_t hobf_nplanes(int32_t nbits) { return (nbits + 3) / 4 * 4; }
+
+int64_t hobf_planes_words(int64_t rows, int64_t c, int32_t nbits) {
+  if (rows < 0 || c < 0) return -1;
+  return rows * ((c + 31) / 32) * hobf_nplanes(nbits);
+}
+
+int32_t hobf_last_launch_count(void) { return g_last_launches; }
+
+const char* hobf_status_str(hobf_status s) {
+  switch (s) {
+    case HOBF_OK: return "ok";
+    case HOBF_EINVAL: return "invalid argument";
+    case HOBF_ESHAPE: return "inconsistent shapes";
+    case HOBF_EUNSUPPORTED: return "unsupported format (no generated kernel)";
+    case HOBF_ECUDA: return "CUDA launch error";
+  }
+  return "unknown status";
+}
+
+const char* hobf_version(void) { return "hobf-b200 0.1 (sm_100a)"; }
+
+static hobf_status pack_common(bool f32, int32_t we, int32_t wf, int32_t rnd, const void* src, int64_t rows,
+                               int64_t c, uint32_t* planes, hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(we, wf) || (f32 && (we > 8 || wf > 23)) || (rnd != 0 && rnd != 1)) return HOBF_EINVAL;
+  if (rows < 0 || c < 0) return HOBF_EINVAL;
+  if (rows == 0 || c == 0) return HOBF_OK;
+  if (!src || !planes || !aligned16(planes)) return HOBF_EINVAL;
+  const int np = hobf_nplanes(3 + we + wf);
+  const int64_t items = rows * ((c + 31) / 32);
+  if (f32)
+    pack_kernel<true><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(src, rows, c, we, wf, rnd, np, planes);
+  else
+    pack_kernel<false><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(src, rows, c, we, wf, 0, np, planes);
+  if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+hobf_status hobf_pack(int32_t we, int32_t wf, const uint32_t* d_words, int64_t rows, int64_t c, uint32_t* d_planes,
+                      hobf_stream stream) {
+  return pack_common(false, we, wf, 0, d_words, rows, c, d_planes, stream);
+}
+
+hobf_status hobf_quantize_pack(int32_t we, int32_t wf, int32_t round, const float* d_x, int64_t rows, int64_t c,
+                               uint32_t* d_planes, hobf_stream stream) {
+  return pack_common(true, we, wf, round, d_x, rows, c, d_planes, stream);
+}
+
+static hobf_status unpack_common(bool f32, int32_t we, int32_t wf, const uint32_t* planes, int64_t rows, int64_t c,
+                                 void* dst, hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(we, wf) || (f32 && (we > 7 || wf > 23))) return HOBF_EINVAL;
+  if (rows < 0 || c < 0) return HOBF_EINVAL;
+  if (rows == 0 || c == 0) return HOBF_OK;
+  if (!planes || !dst || !aligned16(planes)) return HOBF_EINVAL;
+  const int np = hobf_nplanes(3 + we + wf);
+  const int64_t items = rows * ((c + 31) / 32);
+  if (f32)
+    unpack_kernel<true><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(planes, rows, c, we, wf, np, dst);
+  else
+    unpack_kernel<false><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(planes, rows, c, we, wf, np, dst);
+  if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+hobf_status hobf_unpack(int32_t we, int32_t wf, const uint32_t* d_planes, int64_t rows, int64_t c, uint32_t* d_words,
+                        hobf_stream stream) {
+  return unpack_common(false, we, wf, d_planes, rows, c, d_words, stream);
+}
+
+hobf_status hobf_unpack_f32(int32_t we, int32_t wf, const uint32_t* d_planes, int64_t rows, int64_t c, float* d_x,
+                            hobf_stream stream) {
+  return unpack_common(true, we, wf, d_planes, rows, c, d_x, stream);
+}
+
+hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
+                        const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
+                        int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
+    return HOBF_EINVAL;
+  if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)
+    return HOBF_EINVAL;
+  if (h == 0 || w == 0 || cin == 0 || kh == 0 || kw == 0 || cout == 0) return HOBF_ESHAPE;
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
+  const FormatEntry* e = f.extended ? nullptr : find_format(f.we, f.wf, f.round);
+  if (!e) return HOBF_EUNSUPPORTED;
+  if (n == 0) return HOBF_OK;
+  if (!d_x_planes || !d_w_planes || !d_y_planes) return HOBF_EINVAL;
+  if (!aligned16(d_x_planes) || !aligned16(d_w_planes) || !aligned16(d_y_planes)) return HOBF_EINVAL;
+  ConvArgs a;
+  a.x = d_x_planes; a.wt = d_w_planes; a.y = d_y_planes;
+  a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
+  a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
+  a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
+  a.variant = 0;
+  if (e->conv(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+hobf_status hobf_mac_planes(hobf_fmt f, uint32_t* d_acc, const uint32_t* d_a, const uint32_t* d_b, int64_t n_groups,
+                            hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || n_groups < 0) return HOBF_EINVAL;
+  const FormatEntry* e = f.extended ? nullptr : find_format(f.we, f.wf, f.round);
+  if (!e) return HOBF_EUNSUPPORTED;
+  if (n_groups == 0) return HOBF_OK;
+  if (!d_acc || !d_a || !d_b || !aligned16(d_acc) || !aligned16(d_a) || !aligned16(d_b)) return HOBF_EINVAL;
+  if (e->mac(d_acc, d_a, d_b, n_groups, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add, int32_t* relu) {
+  const FormatEntry* e = f.extended ? nullptr : find_format(f.we, f.wf, f.round);
+  if (!e) return HOBF_EUNSUPPORTED;
+  if (mac) *mac = e->g_mac;
+  if (mul) *mul = e->g_mul;
+  if (add) *add = e->g_add;
+  if (relu) *relu = e->g_relu;
+  return HOBF_OK;
+}
+
+hobf_status hobf_lop3_peak(int32_t blocks, int32_t threads, int32_t iters, uint32_t* d_sink, hobf_stream stream,
+                           int64_t* lop3_per_launch) {
+  g_last_launches = 0;
+  if (blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !d_sink) return HOBF_EINVAL;
+  lop3_peak_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(d_sink, 1u, iters);
+  if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
+  if (lop3_per_launch) *lop3_per_launch = (int64_t)blocks * threads * iters * 128;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+}  // extern "C"

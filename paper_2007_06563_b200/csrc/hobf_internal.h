@@ -1,0 +1,26 @@
+// hobf_internal.h -- types shared by the C-ABI layer and the per-format kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hobf {
+
+struct ConvArgs {
+  const uint32_t* x;   // input planes  [n][h][w][ceil(cin/32)][NPI]
+  const uint32_t* wt;  // weight planes [kh][kw][cin][ceil(cout/32)][NPI]
+  uint32_t* y;         // output planes [n][ho][wo][ceil(cout/32)][NPO]
+  int n, h, w, cin, kh, kw, cout, stride, pad, relu, ho, wo;
+  int64_t items;       // n * ho * wo * ceil(cout/32)
+  int variant;         // kernel variant (0 = auto)
+};
+
+typedef cudaError_t (*conv_launcher)(const ConvArgs&, cudaStream_t);
+typedef cudaError_t (*mac_launcher)(uint32_t*, const uint32_t*, const uint32_t*, int64_t, cudaStream_t);
+
+struct FormatEntry {
+  int we, wf, rnd, g_mac, g_mul, g_add, g_relu;
+  conv_launcher conv;
+  mac_launcher mac;
+};
+
+}  // namespace hobf

@@ -1,0 +1,135 @@
+// hobf_kernels.cuh -- format-templated CUDA kernels of the hot path (sm_100a).
+//
+// Instantiated once per generated circuit (csrc/gen/hobf_fmt_*.cu).  F is a
+// generated struct (csrc/gen/hobf_circuit_*.cuh) holding the format constants
+// and the straight-line lop3 MAC / ReLU bodies.
+//
+// Plane layout (L18): a tensor [rows][C] of NBITS-bit words is
+// stored as planes[rows][ceil(C/32)][NP], NP = roundup(NBITS, 4); bit l of
+// word (r, g, j) is field bit j of element (r, 32g + l).  Padding lanes and
+// planes are zero (= canonical +0).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hobf_internal.h"
+
+namespace hobf {
+
+// ---------------------------------------------------------------------------
+// conv2d: one thread = one output pixel x one group of 32 output channels.
+// Lanes of every register are the 32 output channels (the paper's tiling of
+// the M kernels by LANES); the activation value is broadcast across
+// the lanes.  The accumulator (NOUT registers) stays in registers for
+// the whole serial (c, kh, kw) reduction (L10); ReLU is fused (L12).
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
+  const int G = (a.cout + 31) >> 5;
+  const int CG = (a.cin + 31) >> 5;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.items) return;
+  const int g = (int)(t % G);
+  const int64_t pix = t / G;
+  const int ox = (int)(pix % a.wo);
+  const int oy = (int)((pix / a.wo) % a.ho);
+  const int64_t ni = pix / ((int64_t)a.wo * a.ho);
+
+  uint32_t acc[F::NOUT];
+#pragma unroll
+  for (int j = 0; j < F::NOUT; j++) acc[j] = 0u;  // +0 (L9)
+
+  const uint32_t* __restrict__ xbase = a.x + ni * (int64_t)a.h * a.w * CG * F::NPI;
+  const uint32_t* __restrict__ wbase = a.wt + (int64_t)g * F::NPI;
+  const int64_t wstride_c = (int64_t)G * F::NPI;  // next input channel
+#pragma unroll 1
+  for (int c = 0; c < a.cin; c++) {
+    const int cg = c >> 5, b = c & 31;
+#pragma unroll 1
+    for (int kh = 0; kh < a.kh; kh++) {
+      const int iy = oy * a.stride - a.pad + kh;
+#pragma unroll 1
+      for (int kw = 0; kw < a.kw; kw++) {
+        const int ix = ox * a.stride - a.pad + kw;
+        uint32_t X[F::NPI];
+        if (iy >= 0 && iy < a.h && ix >= 0 && ix < a.w) {
+          const uint4* px = reinterpret_cast<const uint4*>(xbase + (((int64_t)iy * a.w + ix) * CG + cg) * F::NPI);
+#pragma unroll
+          for (int q = 0; q < F::NPI / 4; q++) {
+            const uint4 v = __ldg(px + q);
+            X[4 * q + 0] = v.x; X[4 * q + 1] = v.y; X[4 * q + 2] = v.z; X[4 * q + 3] = v.w;
+          }
+#pragma unroll
+          for (int j = 0; j < F::NPI; j++) X[j] = 0u - ((X[j] >> b) & 1u);  // broadcast
+        } else {
+#pragma unroll
+          for (int j = 0; j < F::NPI; j++) X[j] = 0u;  // zero padding = +0 (L11, L14)
+        }
+        uint32_t W[F::NPI];
+        const uint4* pw = reinterpret_cast<const uint4*>(wbase + ((int64_t)(kh * a.kw + kw) * a.cin + c) * wstride_c);
+#pragma unroll
+        for (int q = 0; q < F::NPI / 4; q++) {
+          const uint4 v = __ldg(pw + q);
+          W[4 * q + 0] = v.x; W[4 * q + 1] = v.y; W[4 * q + 2] = v.z; W[4 * q + 3] = v.w;
+        }
+        F::mac(acc, X, W);
+      }
+    }
+  }
+  if (a.relu) F::relu(acc, acc);
+  uint4* py = reinterpret_cast<uint4*>(a.y + t * F::NPO);
+#pragma unroll
+  for (int q = 0; q < F::NPO / 4; q++) {
+    uint4 v;
+    v.x = (4 * q + 0 < F::NOUT) ? acc[(4 * q + 0) % F::NOUT] : 0u;
+    v.y = (4 * q + 1 < F::NOUT) ? acc[(4 * q + 1) % F::NOUT] : 0u;
+    v.z = (4 * q + 2 < F::NOUT) ? acc[(4 * q + 2) % F::NOUT] : 0u;
+    v.w = (4 * q + 3 < F::NOUT) ? acc[(4 * q + 3) % F::NOUT] : 0u;
+    py[q] = v;
+  }
+}
+
+// mac_planes: acc[i] = add(acc[i], mul(a[i], b[i])) lane-wise on plane groups.
+template <class F>
+__global__ void __launch_bounds__(256) mac_planes_kernel(uint32_t* __restrict__ acc_p, const uint32_t* __restrict__ a_p,
+                                                         const uint32_t* __restrict__ b_p, int64_t n_groups) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_groups; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t acc[F::NPO], x[F::NPI], w[F::NPI];
+#pragma unroll
+    for (int j = 0; j < F::NPO; j++) acc[j] = acc_p[i * F::NPO + j];
+#pragma unroll
+    for (int j = 0; j < F::NPI; j++) { x[j] = a_p[i * F::NPI + j]; w[j] = b_p[i * F::NPI + j]; }
+    F::mac(acc, x, w);
+#pragma unroll
+    for (int j = 0; j < F::NPO; j++) acc_p[i * F::NPO + j] = (j < F::NOUT) ? acc[j] : 0u;
+  }
+}
+
+template <class F>
+cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
+  if (a.items == 0) return cudaSuccess;
+  const int threads = 128;
+  const int64_t blocks = (a.items + threads - 1) / threads;
+  conv_direct_kernel<F><<<(unsigned)blocks, threads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <class F>
+cudaError_t launch_mac(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  mac_planes_kernel<F><<<(unsigned)blocks, 256, 0, s>>>(acc, x, w, n);
+  return cudaGetLastError();
+}
+
+}  // namespace hobf
+
+#define HOBF_INSTANTIATE(TAG, WE, WF, RND)                                                                   \
+  cudaError_t hobf_launch_conv_##TAG(const hobf::ConvArgs& a, cudaStream_t s) {                            \
+    return hobf::launch_conv<hobf_gen::F_##TAG>(a, s);                                                      \
+  }                                                                                                         \
+  cudaError_t hobf_launch_mac_##TAG(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n,        \
+                                    cudaStream_t s) {                                                       \
+    return hobf::launch_mac<hobf_gen::F_##TAG>(acc, x, w, n, s);                                            \
+  }

@@ -1,0 +1,372 @@
+"""Gate-level HOBFLOPS floating-point multiplier and adder (the FloPoCo + Genus
+stage of the paper's flow, rebuilt in-repo).
+
+Every circuit is built as an AIG (``aig.AIG``).  Bit vectors are Python lists
+of literals, least significant bit first.
+
+Operand format F(wE, wF): word bits [exc:2 | sign | exp:wE | frac:wF]
+MSB..LSB; exc 00 zero, 01 normal, 10 inf, 11 NaN; significand 1.f; bias
+2^(wE-1)-1; every exponent code is a normal binade (no subnormals).
+Product / accumulator width: wF+1 (single) or 2wF+1 (extended) (Table 4,
+P:151-177).  Rounding: RNE or RTZ.
+
+The circuits assume canonical operands (exc != 01 => exp = frac = 0, NaN
+sign 0), which pack/quantise guarantee and which every circuit output
+satisfies; this don't-care is what lets zero operands flow through the adder
+datapath without a bypass (see ``fp_add``).
+"""
+from __future__ import annotations
+
+from .aig import AIG, FALSE, TRUE
+
+RNE = 0
+RTZ = 1
+
+
+def bias(we: int) -> int:
+    return (1 << (we - 1)) - 1
+
+
+class FP:
+    """Field view of an encoded word given as a list of literals."""
+
+    def __init__(self, bits, we, wf):
+        assert len(bits) == 3 + we + wf
+        self.we, self.wf = we, wf
+        self.frac = bits[0:wf]
+        self.exp = bits[wf:wf + we]
+        self.sign = bits[wf + we]
+        self.exc0 = bits[wf + we + 1]
+        self.exc1 = bits[wf + we + 2]
+
+
+def pack_bits(frac, exp, sign, exc0, exc1):
+    return list(frac) + list(exp) + [sign, exc0, exc1]
+
+
+# --------------------------------------------------------------------------- integer blocks
+
+def ripple_add(g: AIG, a, b, cin=FALSE, width=None):
+    """a + b + cin (LSB first); returns width bits (default max(len)+1)."""
+    n = max(len(a), len(b))
+    if width is None:
+        width = n + 1
+    a = list(a) + [FALSE] * (width - len(a))
+    b = list(b) + [FALSE] * (width - len(b))
+    out = []
+    c = cin
+    for i in range(width):
+        out.append(g.XOR3(a[i], b[i], c))
+        if i < width - 1:
+            c = g.MAJ(a[i], b[i], c)
+    return out
+
+
+def increment(g: AIG, a, inc, width=None):
+    """a + inc (single bit); returns (bits[width], carry_out)."""
+    if width is None:
+        width = len(a)
+    out = []
+    c = inc
+    for i in range(width):
+        ai = a[i] if i < len(a) else FALSE
+        out.append(g.XOR(ai, c))
+        c = g.AND(ai, c)
+    return out, c
+
+
+def const_bits(value: int, width: int):
+    return [TRUE if (value >> i) & 1 else FALSE for i in range(width)]
+
+
+def less_than(g: AIG, a, b):
+    """unsigned a < b (borrow out of a - b)."""
+    br = FALSE
+    for ai, bi in zip(a, b):
+        br = g.MAJ(g.NOT(ai), bi, br)
+    return br
+
+
+def multiply(g: AIG, a, b):
+    """Unsigned array multiplier (AND partial products, column compression with
+    full/half adders, final ripple adder).  Returns len(a)+len(b) bits."""
+    W = len(a) + len(b)
+    cols = [[] for _ in range(W + 1)]
+    for j, bj in enumerate(b):
+        for i, ai in enumerate(a):
+            p = g.AND(ai, bj)
+            if p != FALSE:
+                cols[i + j].append(p)
+    # Dadda-style reduction to two rows
+    while max(len(c) for c in cols) > 2:
+        new = [[] for _ in range(W + 1)]
+        for k in range(W):
+            col = cols[k]
+            while len(col) >= 3:
+                x, y, z = col.pop(0), col.pop(0), col.pop(0)
+                new[k].append(g.XOR3(x, y, z))
+                new[k + 1].append(g.MAJ(x, y, z))
+            new[k].extend(col)
+        cols = new
+    r0 = [c[0] if len(c) > 0 else FALSE for c in cols[:W]]
+    r1 = [c[1] if len(c) > 1 else FALSE for c in cols[:W]]
+    return ripple_add(g, r0, r1, FALSE, width=W)
+
+
+def shift_right_sticky(g: AIG, v, d, order="small_first"):
+    """Logical right shift of v (LSB first) by the unsigned amount d (bits LSB
+    first); returns (shifted, sticky) where sticky = OR of all bits shifted out."""
+    W = len(v)
+    K = 0
+    while (1 << K) <= W:
+        K += 1
+    K = min(K, len(d))
+    big = g.OR_many(d[K:])
+    cur = list(v)
+    sticky = FALSE
+    stages = list(range(K)) if order == "small_first" else list(reversed(range(K)))
+    for j in stages:
+        sh = 1 << j
+        out_bits = g.OR_many(cur[:sh])
+        sticky = g.OR(sticky, g.AND(d[j], out_bits))
+        cur = [g.MUX(d[j], cur[i + sh] if i + sh < W else FALSE, cur[i]) for i in range(W)]
+    if big != FALSE:
+        anyv = g.OR_many(v)
+        sticky = g.MUX(big, anyv, sticky)
+        cur = [g.AND(g.NOT(big), x) for x in cur]
+    return cur, sticky
+
+
+def lzc(g: AIG, v):
+    """Leading-zero count of v (LSB first; leading = from the MSB).  Returns
+    (count bits LSB first, all_zero)."""
+    n = len(v)
+    P = 1
+    while P < n:
+        P *= 2
+    msb_first = list(reversed(v)) + [FALSE] * (P - n)  # pad at the bottom (LSB side)
+
+    def rec(bits):
+        # returns (count bits LSB first over log2(len) bits, zero flag)
+        if len(bits) == 1:
+            return [], g.NOT(bits[0])
+        h = len(bits) // 2
+        ch, zh = rec(bits[:h])
+        cl, zl = rec(bits[h:])
+        cnt = [g.MUX(zh, cl[i], ch[i]) for i in range(len(ch))] + [zh]
+        return cnt, g.AND(zh, zl)
+
+    cnt, z = rec(msb_first)
+    return cnt, z
+
+
+def shift_left(g: AIG, v, s):
+    cur = list(v)
+    W = len(v)
+    for j in reversed(range(len(s))):
+        sh = 1 << j
+        if sh >= W:
+            cur = [g.AND(g.NOT(s[j]), x) for x in cur]
+            continue
+        cur = [g.MUX(s[j], cur[i - sh] if i - sh >= 0 else FALSE, cur[i]) for i in range(W)]
+    return cur
+
+
+# --------------------------------------------------------------------------- FP multiplier
+
+def fp_mul(g: AIG, A: FP, B: FP, wfo: int, rnd: int):
+    """HOBFLOPS multiplier F(wE,wF) x F(wE,wF) -> F(wE,wfo) (Table 4).
+
+    Exception combine, sign XOR, (wF+1)^2 significand product with the hidden
+    bit wired to 1 (non-normal operands are overridden by the exception logic),
+    1-bit normalisation, round to wfo fraction bits (RNE / RTZ), exponent
+    Ea + Eb - bias + norm + round-carry at wE+2 bits, overflow -> inf,
+    underflow -> zero (SURVEY 8(c) mul, ledger L5/L6)."""
+    we, wf = A.we, A.wf
+    assert wfo >= wf
+    nA, nB = g.AND(A.exc1, A.exc0), g.AND(B.exc1, B.exc0)
+    iA, iB = g.AND(A.exc1, g.NOT(A.exc0)), g.AND(B.exc1, g.NOT(B.exc0))
+    zA, zB = g.AND(g.NOT(A.exc1), g.NOT(A.exc0)), g.AND(g.NOT(B.exc1), g.NOT(B.exc0))
+    normA, normB = g.AND(g.NOT(A.exc1), A.exc0), g.AND(g.NOT(B.exc1), B.exc0)
+
+    ma = list(A.frac) + [TRUE]
+    mb = list(B.frac) + [TRUE]
+    P = multiply(g, ma, mb)                    # 2wf+2 bits, value in [1, 4)
+    top = P[2 * wf + 1]
+    # normalised significand N (2wf+2 bits, leading one at 2wf+1)
+    N = [g.MUX(top, P[i], P[i - 1] if i >= 1 else FALSE) for i in range(2 * wf + 2)]
+    keep_lo = 2 * wf + 1 - wfo                 # kept bits N[2wf+1 .. keep_lo] (wfo+1 bits)
+    if keep_lo >= 0:
+        kept = N[keep_lo:2 * wf + 2]
+        if keep_lo >= 1:
+            guard = N[keep_lo - 1]
+            sticky = g.OR_many(N[:keep_lo - 1])
+        else:
+            guard, sticky = FALSE, FALSE
+    else:
+        kept = [FALSE] * (-keep_lo) + N        # extended: exact, zero-fill below
+        guard, sticky = FALSE, FALSE
+    if rnd == RNE and guard != FALSE:
+        inc = g.AND(guard, g.OR(sticky, kept[0]))
+        rounded, rc = increment(g, kept, inc)
+    else:
+        rounded, rc = kept, FALSE
+    frac = rounded[:wfo]                       # if rc, these are all zero already
+
+    # exponent: Ea + Eb - bias + top + rc in wE+2 bits (two's complement)
+    EW = we + 2
+    s1 = ripple_add(g, A.exp, B.exp, top, width=EW)
+    s2 = ripple_add(g, s1, const_bits((1 << EW) - bias(we), EW), FALSE, width=EW)
+    E, _ = increment(g, s2, rc, width=EW)
+    unf = E[EW - 1]
+    ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])   # E >= 2^wE (E < 2^(wE+1) always)
+
+    both = g.AND(normA, normB)
+    nan = g.OR_many([nA, nB, g.AND(iA, zB), g.AND(zA, iB)])
+    normal = g.AND(both, g.AND(g.NOT(ovf), g.NOT(unf)))
+    exc1 = g.OR_many([nan, iA, iB, g.AND(both, ovf)])
+    exc0 = g.OR(nan, normal)
+    sign = g.AND(g.XOR(A.sign, B.sign), g.NOT(nan))
+    exp_out = [g.AND(normal, e) for e in E[:we]]
+    frac_out = [g.AND(normal, f) for f in frac]
+    return pack_bits(frac_out, exp_out, sign, exc0, exc1)
+
+
+# --------------------------------------------------------------------------- FP adder
+
+def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
+    """HOBFLOPS adder F(wE,w) + F(wE,w) -> F(wE,w) (single-path, P:190-198;
+    SURVEY 8(c) add; ledger L5-L7).
+
+    Magnitude compare of (exp, frac) and swap so that |X| >= |Y|; alignment
+    right shift of 1.fY by eX - eY with guard, round and sticky; effective
+    add/subtract; leading-zero count and left normalisation; RNE/RTZ rounding;
+    exponent eX + 1 - lzc + round-carry; overflow -> inf, underflow -> zero,
+    exact cancellation -> +0, (-0) + (-0) -> -0.
+
+    Zero operands are canonical (exp = frac = 0) and get hidden bit 0, so they
+    sort below every normal (or tie with exp=0,frac=0 normals, which share
+    their exponent) and flow through the datapath: 0 + y = y exactly."""
+    we, w = A.we, A.wf
+    p = w + 1
+    nA, nB = g.AND(A.exc1, A.exc0), g.AND(B.exc1, B.exc0)
+    iA, iB = g.AND(A.exc1, g.NOT(A.exc0)), g.AND(B.exc1, g.NOT(B.exc0))
+    hA, hB = g.AND(g.NOT(A.exc1), A.exc0), g.AND(g.NOT(B.exc1), B.exc0)
+    special = g.OR(A.exc1, B.exc1)
+
+    # |A| < |B| by (exp, frac, hidden): the hidden bit as least significant key
+    # breaks the tie between a zero and the exp=0,frac=0 normal in favour of the normal
+    keyA = [hA] + list(A.frac) + list(A.exp)
+    keyB = [hB] + list(B.frac) + list(B.exp)
+    swap = less_than(g, keyA, keyB)
+    eX = [g.MUX(swap, b, a) for a, b in zip(A.exp, B.exp)]
+    eY = [g.MUX(swap, a, b) for a, b in zip(A.exp, B.exp)]
+    fX = [g.MUX(swap, b, a) for a, b in zip(A.frac, B.frac)]
+    fY = [g.MUX(swap, a, b) for a, b in zip(A.frac, B.frac)]
+    hX = g.MUX(swap, hB, hA)
+    hY = g.MUX(swap, hA, hB)
+    sX = g.MUX(swap, B.sign, A.sign)
+    sub = g.XOR(A.sign, B.sign)
+
+    # d = eX - eY >= 0
+    d = ripple_add(g, eX, [g.NOT(x) for x in eY], TRUE, width=we)
+    # alignment: W = p + 2 positions (significand + G + R), then sticky
+    W = p + 2
+    mY = [FALSE, FALSE] + list(fY) + [hY]
+    yv, ys = shift_right_sticky(g, mY, d, order=shift_order)
+    mX = [FALSE, FALSE] + list(fX) + [hX]
+    # adder over W+1 bits: position 0 = sticky, 1..W = shifted significand
+    xo = [FALSE] + mX
+    yo = [g.XOR(ys, sub)] + [g.XOR(b, sub) for b in yv]
+    Z = ripple_add(g, xo, yo, sub, width=W + 2)  # Z[W+1] = carry (add) / discard (sub)
+    Z[W + 1] = g.AND(Z[W + 1], g.NOT(sub))
+    # normalise: leading-zero count over Z[W+1..0]
+    cnt, zsum = lzc(g, Z)
+    Zn = shift_left(g, Z, cnt)
+    # kept p bits: Zn[W+1 .. W+2-p] = Zn[p+3 .. 4]; guard Zn[3]; sticky Zn[2..0]
+    kept = Zn[4:p + 4]
+    guard = Zn[3]
+    sticky = g.OR_many(Zn[0:3])
+    if rnd == RNE:
+        inc = g.AND(guard, g.OR(sticky, kept[0]))
+        rounded, rc = increment(g, kept, inc)
+    else:
+        rounded, rc = kept, FALSE
+    frac = rounded[:w]
+    # exponent: eX + 1 - cnt + rc  (wE+2 bits two's complement)
+    EW = we + 2
+    ncnt = [g.NOT(c) for c in cnt] + [TRUE] * (EW - len(cnt))  # ~cnt sign-extended
+    t = ripple_add(g, eX, ncnt, TRUE, width=EW)                # eX - cnt
+    E = ripple_add(g, t, const_bits(1, EW), rc, width=EW)
+    unf = E[EW - 1]
+    ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])
+
+    nan = g.OR_many([nA, nB, g.AND(g.AND(iA, iB), sub)])
+    fin_nz = g.AND(g.NOT(special), g.NOT(zsum))
+    normal = g.AND(fin_nz, g.AND(g.NOT(ovf), g.NOT(unf)))
+    exc1 = g.OR(special, g.AND(fin_nz, ovf))
+    exc0 = g.OR(nan, normal)
+    zero_sign = g.AND(g.AND(A.sign, B.sign), g.NOT(hA))
+    inf_sign = g.MUX(iA, A.sign, B.sign)
+    sign_fin = g.MUX(zsum, zero_sign, sX)
+    sign = g.AND(g.NOT(nan), g.MUX(special, inf_sign, sign_fin))
+    exp_out = [g.AND(normal, e) for e in E[:we]]
+    frac_out = [g.AND(normal, f) for f in frac]
+    return pack_bits(frac_out, exp_out, sign, exc0, exc1)
+
+
+def fp_relu(g: AIG, A: FP):
+    """ReLU on a canonical word: NaN (sign 0) passes, any word with
+    sign 1 (negative, -0, -inf) becomes +0 (all bits zero), else unchanged."""
+    ns = g.NOT(A.sign)
+    bits = list(A.frac) + list(A.exp) + [A.sign, A.exc0, A.exc1]
+    return [g.AND(ns, b) for b in bits[:-3]] + [FALSE, g.AND(ns, A.exc0), g.AND(ns, A.exc1)]
+
+
+# --------------------------------------------------------------------------- circuits
+
+class Circuit:
+    """A built circuit: AIG, named input vectors and output literals."""
+
+    def __init__(self, name, g, inputs, outputs):
+        self.name = name
+        self.g = g
+        self.inputs = inputs      # list of (name, width)
+        self.outputs = outputs    # list of literals
+
+
+def build_mul(we, wf, wfo, rnd) -> Circuit:
+    g = AIG()
+    a = g.inputs("a", 3 + we + wf)
+    b = g.inputs("b", 3 + we + wf)
+    out = fp_mul(g, FP(a, we, wf), FP(b, we, wf), wfo, rnd)
+    return Circuit(f"mul_e{we}m{wf}_o{wfo}_{'rne' if rnd == RNE else 'rtz'}", g,
+                   [("a", 3 + we + wf), ("b", 3 + we + wf)], out)
+
+
+def build_add(we, w, rnd, **kw) -> Circuit:
+    g = AIG()
+    a = g.inputs("a", 3 + we + w)
+    b = g.inputs("b", 3 + we + w)
+    out = fp_add(g, FP(a, we, w), FP(b, we, w), rnd, **kw)
+    return Circuit(f"add_e{we}m{w}_{'rne' if rnd == RNE else 'rtz'}", g,
+                   [("a", 3 + we + w), ("b", 3 + we + w)], out)
+
+
+def build_mac(we, wf, wfo, rnd, **kw) -> Circuit:
+    """acc' = add(acc, mul(x, w)) -- one step of the conv reduction."""
+    g = AIG()
+    acc = g.inputs("acc", 3 + we + wfo)
+    x = g.inputs("x", 3 + we + wf)
+    w = g.inputs("w", 3 + we + wf)
+    p = fp_mul(g, FP(x, we, wf), FP(w, we, wf), wfo, rnd)
+    out = fp_add(g, FP(acc, we, wfo), FP(p, we, wfo), rnd, **kw)
+    return Circuit(f"mac_e{we}m{wf}_{'rne' if rnd == RNE else 'rtz'}", g,
+                   [("acc", 3 + we + wfo), ("x", 3 + we + wf), ("w", 3 + we + wf)], out)
+
+
+def build_relu(we, w) -> Circuit:
+    g = AIG()
+    a = g.inputs("a", 3 + we + w)
+    out = fp_relu(g, FP(a, we, w))
+    return Circuit(f"relu_e{we}m{w}", g, [("a", 3 + we + w)], out)

@@ -1,0 +1,242 @@
+"""Thin Python binding of the C ABI in ``include/hobf.h`` (``libhobf.so``).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C ABI.  Tensors are torch CUDA tensors; bit patterns are
+carried in ``torch.int32`` tensors (same bits as the ABI's uint32).  There is
+no CPU fallback: if the shared library is missing this module raises on import.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhobf.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(or `make -C paper_2007_06563_b200/csrc -j`)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+RNE = 0
+RTZ = 1
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "inconsistent shapes", 3: "unsupported format", 4: "CUDA launch error"}
+
+
+class HobfError(RuntimeError):
+    def __init__(self, fn, status):
+        super().__init__(f"{fn}: {STATUS.get(status, status)} (status {status})")
+        self.status = status
+
+
+class hobf_fmt(ctypes.Structure):
+    _fields_ = [("we", ctypes.c_int32), ("wf", ctypes.c_int32), ("round", ctypes.c_int32), ("extended", ctypes.c_int32)]
+
+
+@dataclass(frozen=True)
+class Fmt:
+    """Input format F(we, wf) plus MAC mode (round: 0 RNE / 1 RTZ; extended: 0 single)."""
+    we: int
+    wf: int
+    round: int = RNE
+    extended: int = 0
+
+    def c(self) -> hobf_fmt:
+        return hobf_fmt(self.we, self.wf, self.round, self.extended)
+
+    @property
+    def nin(self) -> int:
+        return 3 + self.we + self.wf
+
+    @property
+    def wfo(self) -> int:
+        return 2 * self.wf + 1 if self.extended else self.wf + 1
+
+    @property
+    def nout(self) -> int:
+        return 3 + self.we + self.wfo
+
+
+_i32, _i64, _p = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+_lib.hobf_nbits.restype = _i32
+_lib.hobf_nbits.argtypes = [_i32, _i32]
+_lib.hobf_out_wf.restype = _i32
+_lib.hobf_out_wf.argtypes = [hobf_fmt]
+_lib.hobf_nplanes.restype = _i32
+_lib.hobf_nplanes.argtypes = [_i32]
+_lib.hobf_planes_words.restype = _i64
+_lib.hobf_planes_words.argtypes = [_i64, _i64, _i32]
+for _name in ("hobf_pack", "hobf_unpack"):
+    getattr(_lib, _name).restype = _i32
+    getattr(_lib, _name).argtypes = [_i32, _i32, _p, _i64, _i64, _p, _p]
+_lib.hobf_quantize_pack.restype = _i32
+_lib.hobf_quantize_pack.argtypes = [_i32, _i32, _i32, _p, _i64, _i64, _p, _p]
+_lib.hobf_unpack_f32.restype = _i32
+_lib.hobf_unpack_f32.argtypes = [_i32, _i32, _p, _i64, _i64, _p, _p]
+_lib.hobf_conv2d.restype = _i32
+_lib.hobf_conv2d.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _i32, _p, _p]
+_lib.hobf_mac_planes.restype = _i32
+_lib.hobf_mac_planes.argtypes = [hobf_fmt, _p, _p, _p, _i64, _p]
+_lib.hobf_gate_count.restype = _i32
+_lib.hobf_gate_count.argtypes = [hobf_fmt, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                                 ctypes.POINTER(_i32)]
+_lib.hobf_lop3_peak.restype = _i32
+_lib.hobf_lop3_peak.argtypes = [_i32, _i32, _i32, _p, _p, ctypes.POINTER(_i64)]
+_lib.hobf_last_launch_count.restype = _i32
+_lib.hobf_status_str.restype = ctypes.c_char_p
+_lib.hobf_status_str.argtypes = [_i32]
+_lib.hobf_version.restype = ctypes.c_char_p
+
+SYMBOLS = ["hobf_nbits", "hobf_out_wf", "hobf_nplanes", "hobf_planes_words", "hobf_pack", "hobf_quantize_pack",
+           "hobf_unpack", "hobf_unpack_f32", "hobf_conv2d", "hobf_mac_planes", "hobf_gate_count",
+           "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version"]
+
+
+def _check(fn, st):
+    if st != 0:
+        raise HobfError(fn, st)
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def nbits(we: int, wf: int) -> int:
+    return _lib.hobf_nbits(we, wf)
+
+
+def nplanes(nb: int) -> int:
+    return _lib.hobf_nplanes(nb)
+
+
+def planes_words(rows: int, c: int, nb: int) -> int:
+    return _lib.hobf_planes_words(rows, c, nb)
+
+
+def planes_shape(rows: int, c: int, nb: int):
+    return (rows, (c + 31) // 32, nplanes(nb))
+
+
+def last_launch_count() -> int:
+    return _lib.hobf_last_launch_count()
+
+
+def version() -> str:
+    return _lib.hobf_version().decode()
+
+
+def _new_planes(rows, c, nb, device, out=None):
+    shape = planes_shape(rows, c, nb)
+    if out is None:
+        return torch.empty(shape, dtype=torch.int32, device=device)
+    assert out.numel() == shape[0] * shape[1] * shape[2] and out.dtype == torch.int32
+    return out
+
+
+def pack(we: int, wf: int, words: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """words [rows, c] (int32 bit patterns, CUDA) -> planes [rows, ceil(c/32), NP]."""
+    assert words.is_cuda and words.dtype == torch.int32 and words.is_contiguous()
+    rows, c = words.shape
+    out = _new_planes(rows, c, nbits(we, wf), words.device, out)
+    _check("hobf_pack", _lib.hobf_pack(we, wf, _ptr(words), rows, c, _ptr(out), _stream(stream)))
+    return out
+
+
+def quantize_pack(we: int, wf: int, x: torch.Tensor, rnd: int = RNE, out=None, stream=None) -> torch.Tensor:
+    """float32 [rows, c] (CUDA) -> planes in F(we, wf), quantised with rnd."""
+    assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+    rows, c = x.shape
+    out = _new_planes(rows, c, nbits(we, wf), x.device, out)
+    _check("hobf_quantize_pack", _lib.hobf_quantize_pack(we, wf, rnd, _ptr(x), rows, c, _ptr(out), _stream(stream)))
+    return out
+
+
+def unpack(we: int, wf: int, planes: torch.Tensor, rows: int, c: int, out=None, stream=None) -> torch.Tensor:
+    assert planes.is_cuda and planes.dtype == torch.int32 and planes.is_contiguous()
+    if out is None:
+        out = torch.empty((rows, c), dtype=torch.int32, device=planes.device)
+    _check("hobf_unpack", _lib.hobf_unpack(we, wf, _ptr(planes), rows, c, _ptr(out), _stream(stream)))
+    return out
+
+
+def unpack_f32(we: int, wf: int, planes: torch.Tensor, rows: int, c: int, out=None, stream=None) -> torch.Tensor:
+    assert planes.is_cuda and planes.dtype == torch.int32 and planes.is_contiguous()
+    if out is None:
+        out = torch.empty((rows, c), dtype=torch.float32, device=planes.device)
+    _check("hobf_unpack_f32", _lib.hobf_unpack_f32(we, wf, _ptr(planes), rows, c, _ptr(out), _stream(stream)))
+    return out
+
+
+def conv_out_hw(h, w, kh, kw, stride, pad):
+    return (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
+
+
+def conv2d(f: Fmt, x_planes: torch.Tensor, n: int, h: int, w: int, cin: int, w_planes: torch.Tensor,
+           kh: int, kw: int, cout: int, stride: int = 1, pad: int = 1, relu: int = 0, out=None,
+           stream=None) -> torch.Tensor:
+    """HOBFLOPS conv on planes; returns output planes [n*ho*wo, ceil(cout/32), NP(NOUT)]."""
+    ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
+    dev = x_planes.device
+    out = _new_planes(max(n * ho * wo, 0), cout, f.nout, dev, out)
+    _check("hobf_conv2d", _lib.hobf_conv2d(f.c(), _ptr(x_planes), n, h, w, cin, _ptr(w_planes), kh, kw, cout,
+                                           stride, pad, int(relu), _ptr(out), _stream(stream)))
+    return out
+
+
+def mac_planes(f: Fmt, acc: torch.Tensor, a: torch.Tensor, b: torch.Tensor, stream=None) -> torch.Tensor:
+    """In place: acc = add(acc, mul(a, b)) lane-wise. acc [G, NP(NOUT)], a/b [G, NP(NIN)]."""
+    n = acc.shape[0]
+    assert a.shape[0] == n and b.shape[0] == n
+    _check("hobf_mac_planes", _lib.hobf_mac_planes(f.c(), _ptr(acc), _ptr(a), _ptr(b), n, _stream(stream)))
+    return acc
+
+
+def gate_count(f: Fmt) -> dict:
+    v = [_i32() for _ in range(4)]
+    _check("hobf_gate_count", _lib.hobf_gate_count(f.c(), *[ctypes.byref(x) for x in v]))
+    return {"mac": v[0].value, "mul": v[1].value, "add": v[2].value, "relu": v[3].value}
+
+
+def lop3_peak(blocks: int, threads: int, iters: int, sink: torch.Tensor, stream=None) -> int:
+    n = _i64()
+    _check("hobf_lop3_peak", _lib.hobf_lop3_peak(blocks, threads, iters, _ptr(sink), _stream(stream), ctypes.byref(n)))
+    return n.value
+
+
+class Conv2d:
+    """User-level HOBFLOPS convolution layer (the public API a user calls).
+
+    Weights are quantised and bitsliced once at construction (the paper keeps
+    kernels pre-transformed); ``__call__`` quantises + packs the float32
+    NHWC input, runs the bitsliced conv and unpacks the NHWC float32 output
+    (exact in float32), all in CUDA kernels."""
+
+    def __init__(self, weight_f32: torch.Tensor, f: Fmt, stride: int = 1, pad: int = 1, relu: bool = False):
+        kh, kw, cin, cout = weight_f32.shape
+        self.f, self.kh, self.kw, self.cin, self.cout = f, kh, kw, cin, cout
+        self.stride, self.pad, self.relu = stride, pad, relu
+        self.w_planes = quantize_pack(f.we, f.wf, weight_f32.reshape(kh * kw * cin, cout).contiguous(), f.round)
+
+    def forward_planes(self, x_planes, n, h, w, out=None, stream=None):
+        return conv2d(self.f, x_planes, n, h, w, self.cin, self.w_planes, self.kh, self.kw, self.cout,
+                      self.stride, self.pad, int(self.relu), out=out, stream=stream)
+
+    def __call__(self, x_f32: torch.Tensor) -> torch.Tensor:
+        n, h, w, cin = x_f32.shape
+        assert cin == self.cin
+        xp = quantize_pack(self.f.we, self.f.wf, x_f32.reshape(n * h * w, cin).contiguous(), self.f.round)
+        yp = self.forward_planes(xp, n, h, w)
+        ho, wo = conv_out_hw(h, w, self.kh, self.kw, self.stride, self.pad)
+        y = unpack_f32(self.f.we, self.f.wfo, yp, n * ho * wo, self.cout)
+        return y.reshape(n, ho, wo, self.cout)

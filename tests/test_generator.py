@@ -1,0 +1,186 @@
+"""The LOP3 circuit generator, checked on CPU (no GPU): the AIG and the mapped
+LOP3 network are simulated word-parallel (numpy uint64 bit planes) and
+compared bit-exactly with the oracle -- exhaustively for the <= 9-bit input
+formats, on random + directed vectors above (SURVEY 4 ladder step 3)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import pyref
+from paper_2007_06563_b200.gen import aig as aigmod, bitsim, emit, fpgen, lutmap
+
+
+def canon_words(we, wf):
+    return np.array(pyref.canonical_words(we, wf), dtype=np.uint32)
+
+
+# ----------------------------------------------------------------------------- paper pins for the mapper
+
+def test_full_adder_maps_to_two_lop3():
+    """P:119 / P:241-244: the full adder is two 3-input LUT cells on AVX512
+    (LUT150 = xor3 sum, LUT232 = majority carry); lop3 is the same library."""
+    g = aigmod.AIG()
+    a, b, c = g.input("a"), g.input("b"), g.input("c")
+    s, co = g.XOR3(a, b, c), g.MAJ(a, b, c)
+    m = lutmap.map_aig(g, [s, co])
+    assert m.n_luts == 2
+    tt_of = {v: tt for v, _, tt in m.luts}
+    tts = sorted(tt_of[o >> 1] ^ (0xFF if o & 1 else 0) for o in (s, co))
+    assert tts == sorted([0x96, 0xE8])  # same immediates as LUT150 / LUT232
+
+
+def test_two_bit_adder_maps_to_four_lop3():
+    """Alg. 2: a 2-bit ripple adder with carry-in in 4 LUT3 ops."""
+    g = aigmod.AIG()
+    x = [g.input("x0"), g.input("x1")]
+    y = [g.input("y0"), g.input("y1")]
+    cin = g.input("cin")
+    out = fpgen.ripple_add(g, x, y, cin, width=3)
+    m = lutmap.map_aig(g, out)
+    assert m.n_luts == 4
+    # exhaustive check of the mapped network
+    vals = np.arange(32, dtype=np.uint32)
+    words = {}
+    for i, name in enumerate(["x0", "x1", "y0", "y1", "cin"]):
+        words[name] = np.array([sum(((int(v) >> i) & 1) << k for k, v in enumerate(vals))], dtype=np.uint64)
+    outs = lutmap.simulate_mapping(m, words, np)
+    for k, v in enumerate(vals):
+        v = int(v)
+        xv, yv, cv = (v & 1) | ((v >> 1) & 1) << 1, ((v >> 2) & 1) | ((v >> 3) & 1) << 1, (v >> 4) & 1
+        s = xv + yv + cv
+        got = sum((((int(o[0]) >> k) & 1) << i) for i, o in enumerate(outs))
+        assert got == s
+
+
+def test_lop3_truth_table_convention():
+    """lop3 immediate index = 4a + 2b + c with a=0xF0, b=0xCC, c=0xAA (PTX; Table 2 LUTnnn)."""
+    ones = np.uint64(0xFFFFFFFFFFFFFFFF)
+    a, b, c = np.uint64(0xF0), np.uint64(0xCC), np.uint64(0xAA)
+    for imm in (0x96, 0xE8, 0x01, 0xFE, 0x80, 0x2A):
+        assert int(lutmap.lop3_eval(imm, a, b, c, ones)) & 0xFF == imm
+
+
+# ----------------------------------------------------------------------------- circuits vs oracle
+
+def _check(circuit, mapping, arrays, expected):
+    got_aig = bitsim.run_aig(circuit, arrays)
+    assert np.array_equal(got_aig, expected), "AIG differs from oracle"
+    got_map = bitsim.run_mapping(circuit, mapping, arrays)
+    assert np.array_equal(got_map, expected), "LOP3 mapping differs from oracle"
+
+
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 3), (5, 2), (6, 2), (4, 2)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mul_exhaustive(we, wf, rnd):
+    c = fpgen.build_mul(we, wf, wf + 1, rnd)
+    m = lutmap.map_aig(c.g, c.outputs)
+    w = canon_words(we, wf)
+    A, B = np.meshgrid(w, w, indexing="ij")
+    A, B = A.ravel(), B.ravel()
+    _check(c, m, [A, B], oracle.mul(A, B, we, wf, wf + 1, rnd))
+
+
+@pytest.mark.parametrize("we,w", [(5, 4), (4, 4), (5, 3), (6, 3)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_add_exhaustive(we, w, rnd):
+    c = fpgen.build_add(we, w, rnd)
+    m = lutmap.map_aig(c.g, c.outputs)
+    x = canon_words(we, w)
+    A, B = np.meshgrid(x, x, indexing="ij")
+    A, B = A.ravel(), B.ravel()
+    _check(c, m, [A, B], oracle.add(A, B, we, w, rnd))
+
+
+def _rand_words(rng, n, we, wf, special_frac=0.05):
+    s = rng.integers(0, 2, n)
+    e = rng.integers(0, 1 << we, n)
+    f = rng.integers(0, 1 << wf, n)
+    w = ((1 << (wf + we + 1)) | (s << (wf + we)) | (e << wf) | f).astype(np.uint32)
+    sp = rng.random(n) < special_frac
+    specials = np.array([0, 1 << (wf + we), 2 << (wf + we + 1), (2 << (wf + we + 1)) | (1 << (wf + we)),
+                         3 << (wf + we + 1)], np.uint32)
+    w[sp] = rng.choice(specials, int(sp.sum()))
+    return w
+
+
+@pytest.mark.parametrize("we,wf", [(5, 10), (6, 10), (4, 10), (4, 7), (6, 5)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mac_random_wide(we, wf, rnd):
+    rng = np.random.default_rng(we * 31 + wf * 7 + rnd)
+    N = 200_000
+    c = fpgen.build_mac(we, wf, wf + 1, rnd)
+    m = lutmap.map_aig(c.g, c.outputs)
+    acc = _rand_words(rng, N, we, wf + 1)
+    x = _rand_words(rng, N, we, wf)
+    w = _rand_words(rng, N, we, wf)
+    half = N // 2
+    p = oracle.mul(x[:half], w[:half], we, wf, wf + 1, rnd)
+    acc[:half] = np.where(rng.random(half) < 0.5, p ^ np.uint32(1 << (wf + 1 + we)), acc[:half])
+    _check(c, m, [acc, x, w], oracle.mac(acc, x, w, we, wf, wf + 1, rnd))
+
+
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mac_exhaustive_pairs_e4m3(rnd):
+    """All (x, w) pairs of e4m3 against a spread of accumulators."""
+    we, wf = 4, 3
+    c = fpgen.build_mac(we, wf, wf + 1, rnd)
+    m = lutmap.map_aig(c.g, c.outputs)
+    xi = canon_words(we, wf)
+    X, W = np.meshgrid(xi, xi, indexing="ij")
+    X, W = X.ravel(), W.ravel()
+    accs = canon_words(we, wf + 1)[::37]
+    A = np.repeat(accs, X.size)
+    XX, WW = np.tile(X, accs.size), np.tile(W, accs.size)
+    _check(c, m, [A, XX, WW], oracle.mac(A, XX, WW, we, wf, wf + 1, rnd))
+
+
+def test_relu_circuit():
+    for we, w in [(5, 4), (4, 11)]:
+        c = fpgen.build_relu(we, w)
+        m = lutmap.map_aig(c.g, c.outputs)
+        x = canon_words(we, w) if w < 6 else _rand_words(np.random.default_rng(0), 50000, we, w, 0.2)
+        _check(c, m, [x], oracle.relu(x, we, w))
+
+
+# ----------------------------------------------------------------------------- gate-count properties
+
+def test_gate_count_properties():
+    """RTZ adder < RNE adder for every format; counts
+    non-decreasing in wF at fixed wE (Figs. 8/10/12 trend); the e5m2
+    MAC is within the paper's AVX512 bar of 53 + 204 = 257."""
+    counts = {}
+    for we in (4, 5, 6):
+        for wf in range(2, 11):
+            for rnd in (0, 1):
+                ca = fpgen.build_add(we, wf + 1, rnd)
+                cm = fpgen.build_mul(we, wf, wf + 1, rnd)
+                counts[(we, wf, rnd)] = (lutmap.map_aig(cm.g, cm.outputs).n_luts,
+                                         lutmap.map_aig(ca.g, ca.outputs).n_luts)
+    for we in (4, 5, 6):
+        for wf in range(2, 11):
+            assert counts[(we, wf, 1)][1] < counts[(we, wf, 0)][1]
+            if wf > 2:
+                for rnd in (0, 1):
+                    assert sum(counts[(we, wf, rnd)]) >= sum(counts[(we, wf - 1, rnd)])
+    assert sum(counts[(5, 2, 0)]) <= 257
+
+
+# ----------------------------------------------------------------------------- emitted sources
+
+def test_emitted_headers_up_to_date(tmp_path):
+    """The committed csrc/gen/ sources are exactly what the generator emits."""
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    gen_dir = os.path.join(here, "paper_2007_06563_b200", "csrc", "gen")
+    emit.write_all(str(tmp_path), formats=[(5, 3), (4, 10)])
+    for name in ["hobf_circuit_e5m3_rne.cuh", "hobf_circuit_e4m10_rtz.cuh", "hobf_fmt_e5m3.cu"]:
+        assert open(os.path.join(gen_dir, name)).read() == open(os.path.join(tmp_path, name)).read(), name
+    counts = json.load(open(os.path.join(gen_dir, "gate_counts.json")))
+    assert len(counts) == 54
+
+
+def test_emitted_mac_lop3_count_matches_mapping():
+    r = emit.gen_format(5, 3, 0)
+    assert r["src"].count("hobf_lop3<") == r["g_mac"] + r["g_relu"]

@@ -1,0 +1,307 @@
+"""CUDA path vs oracle, bit-exact, through the C ABI (-m gpu).
+
+Every comparison is on uint32 words: the GPU result is unpacked by the GPU
+unpack kernel and compared element by element with the oracle's words.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import pyref
+from gpu_util import hobf, to_dev_words, to_np_words, group_planes, ungroup_planes
+from paper_2007_06563_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+SWEEP = [(we, wf) for we in (4, 5, 6) for wf in range(2, 11)]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def special_floats():
+    return np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, -1.0, 1e-45, -1e-45, 3.4e38, -3.4e38,
+                     2.0 ** -15, 2.0 ** -16, 131008.0, 131072.0, 65504.0, 480.0, 464.0, 0.1, 2.1875],
+                    dtype=np.float32)
+
+
+# ----------------------------------------------------------------------------- quantise / pack / unpack
+
+@pytest.mark.parametrize("we,wf", [(5, 10), (5, 3), (4, 3), (6, 2), (4, 10), (6, 9), (5, 2)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_quantize_pack_unpack_matches_oracle_encode(we, wf, rnd):
+    H = hobf()
+    rng = np.random.default_rng(we * 100 + wf + rnd)
+    x = (rng.standard_normal(50_000) * np.exp(rng.uniform(-25, 25, 50_000))).astype(np.float32)
+    x = np.concatenate([x, special_floats()])
+    for rows, c in [(x.size // 50, 50), (1, x.size), (x.size // 20, 20)]:
+        xx = x[: rows * c].reshape(rows, c)
+        planes = H.quantize_pack(we, wf, torch.from_numpy(xx).cuda(), rnd)
+        got = to_np_words(H.unpack(we, wf, planes, rows, c))
+        exp = oracle.encode_f32(xx, we, wf, rnd)
+        assert np.array_equal(got, exp)
+        # unpack to float32 is the exact decoded value
+        f = H.unpack_f32(we, wf, planes, rows, c).cpu().numpy()
+        dec = oracle.decode_f64(exp, we, wf)
+        both_nan = np.isnan(f) & np.isnan(dec)
+        assert np.array_equal(f[~both_nan].astype(np.float64), dec[~both_nan])
+        assert np.array_equal(np.signbit(f[~both_nan]), np.signbit(dec[~both_nan]))
+
+
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 10), (6, 5)])
+def test_pack_canonicalises_and_round_trips(we, wf):
+    H = hobf()
+    rng = np.random.default_rng(11)
+    rows, c = 333, 77  # ragged lanes
+    raw = rng.integers(0, 1 << 32, (rows, c), dtype=np.uint64).astype(np.uint32)
+    planes = H.pack(we, wf, to_dev_words(raw))
+    assert tuple(planes.shape) == (rows, 3, H.nplanes(3 + we + wf))
+    got = to_np_words(H.unpack(we, wf, planes, rows, c))
+    nb = 3 + we + wf
+    exp = oracle.canon(raw & np.uint32((1 << nb) - 1), we, wf)
+    assert np.array_equal(got, exp)
+    # padding lanes (c=77 -> lanes 13..31 of group 2) and padding planes are zero
+    p = to_np_words(planes)
+    assert np.all((p[:, 2, :] >> np.uint32(13)) == 0)
+    assert np.all(p[:, :, nb:] == 0)
+    # lane/bit layout (L18): bit l of plane j is bit j of element 32g+l
+    canon = exp
+    for (r, g, j, l) in [(0, 0, 0, 0), (5, 1, 3, 17), (332, 2, nb - 1, 12)]:
+        assert ((p[r, g, j] >> l) & 1) == ((canon[r, 32 * g + l] >> j) & 1)
+
+
+def test_empty_and_error_paths():
+    H = hobf()
+    f = H.Fmt(5, 3)
+    z = torch.zeros((0, 5), dtype=torch.int32, device="cuda")
+    out = H.pack(5, 3, z)
+    assert out.numel() == 0
+    with pytest.raises(H.HobfError) as e:
+        H.gate_count(H.Fmt(7, 3))
+    assert e.value.status == 3
+    with pytest.raises(H.HobfError) as e:
+        H.conv2d(H.Fmt(5, 3, extended=1), torch.zeros(64, dtype=torch.int32, device="cuda"), 1, 2, 2, 1,
+                 torch.zeros(64, dtype=torch.int32, device="cuda"), 3, 3, 1)
+    assert e.value.status == 3
+    with pytest.raises(H.HobfError) as e:  # kernel larger than padded input
+        H.conv2d(f, torch.zeros(64, dtype=torch.int32, device="cuda"), 1, 1, 1, 1,
+                 torch.zeros(64, dtype=torch.int32, device="cuda"), 5, 5, 1, 1, 1)
+    assert e.value.status == 2
+    # n = 0 is a no-op
+    y = H.conv2d(f, torch.zeros(64, dtype=torch.int32, device="cuda"), 0, 4, 4, 8,
+                 torch.zeros(9 * 8 * 12, dtype=torch.int32, device="cuda"), 3, 3, 32)
+    assert y.numel() == 0
+
+
+# ----------------------------------------------------------------------------- MAC circuits
+
+def canon_words(we, wf):
+    return np.array(pyref.canonical_words(we, wf), dtype=np.uint32)
+
+
+def run_mac(f, acc, a, b):
+    """acc/a/b: 1-D words (same length, multiple of 32) -> GPU mac result words."""
+    H = hobf()
+    n = acc.size
+    pa = group_planes(acc, f.we, f.wfo)
+    pa = pa.contiguous()
+    px = group_planes(a, f.we, f.wf)
+    pw = group_planes(b, f.we, f.wf)
+    H.mac_planes(f, pa, px, pw)
+    return ungroup_planes(pa, f.we, f.wfo, n)
+
+
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mac_exhaustive_e5m3(rnd):
+    """Every (acc, x, w) triple of canonical e5m3 operands / e5m4 accumulators:
+    1029 x 517^2 = 2.75e8 MACs (ladder step 5)."""
+    H = hobf()
+    f = H.Fmt(5, 3, rnd)
+    wi = canon_words(5, 3)
+    wo = canon_words(5, 4)
+    X, W = np.meshgrid(wi, wi, indexing="ij")
+    X, W = X.ravel(), W.ravel()                     # 267,289 pairs
+    pad = (-X.size) % 32
+    X = np.concatenate([X, np.zeros(pad, np.uint32)])
+    W = np.concatenate([W, np.zeros(pad, np.uint32)])
+    chunk = 16
+    for s in range(0, wo.size, chunk):
+        accs = wo[s:s + chunk]
+        A = np.repeat(accs, X.size)
+        XX = np.tile(X, accs.size)
+        WW = np.tile(W, accs.size)
+        got = run_mac(f, A, XX, WW)
+        exp = oracle.mac(A, XX, WW, 5, 3, 4, rnd)
+        bad = np.nonzero(got != exp)[0]
+        assert bad.size == 0, [(hex(A[i]), hex(XX[i]), hex(WW[i]), hex(got[i]), hex(exp[i])) for i in bad[:5]]
+
+
+@pytest.mark.parametrize("we,wf", SWEEP)
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mac_random_all_formats(we, wf, rnd):
+    H = hobf()
+    f = H.Fmt(we, wf, rnd)
+    rng = np.random.default_rng(we * 1000 + wf * 10 + rnd)
+    N = 1 << 18
+
+    def rand_words(wfx, n):
+        s = rng.integers(0, 2, n)
+        e = rng.integers(0, 1 << we, n)
+        fr = rng.integers(0, 1 << wfx, n)
+        w = ((1 << (wfx + we + 1)) | (s << (wfx + we)) | (e << wfx) | fr).astype(np.uint32)
+        # sprinkle specials (zero, -0, inf, -inf, nan)
+        sp = rng.random(n) < 0.05
+        specials = np.array(pyref.canonical_words(we, 1)[:5], np.uint32)
+        specials = np.array([0, 1 << (wfx + we), 2 << (wfx + we + 1), (2 << (wfx + we + 1)) | (1 << (wfx + we)),
+                             3 << (wfx + we + 1)], np.uint32)
+        w[sp] = rng.choice(specials, sp.sum())
+        return w
+
+    A = rand_words(wf + 1, N)
+    X = rand_words(wf, N)
+    Wt = rand_words(wf, N)
+    # half the accumulators near the product magnitude so cancellation / rounding paths are hit
+    half = N // 2
+    prod = oracle.mul(X[:half], Wt[:half], we, wf, wf + 1, rnd)
+    A[:half] = np.where(rng.random(half) < 0.5, prod ^ np.uint32(1 << (wf + 1 + we)), A[:half])
+    got = run_mac(f, A, X, Wt)
+    exp = oracle.mac(A, X, Wt, we, wf, wf + 1, rnd)
+    bad = np.nonzero(got != exp)[0]
+    assert bad.size == 0, [(hex(A[i]), hex(X[i]), hex(Wt[i]), hex(got[i]), hex(exp[i])) for i in bad[:5]]
+
+
+def test_gate_counts_reported():
+    H = hobf()
+    import json, os
+    path = os.path.join(os.path.dirname(H.LIB_PATH), "csrc", "gen", "gate_counts.json")
+    counts = json.load(open(path))
+    for (we, wf) in SWEEP:
+        for rnd, name in ((0, "rne"), (1, "rtz")):
+            g = H.gate_count(H.Fmt(we, wf, rnd))
+            assert g["mac"] == counts[f"e{we}m{wf}_{name}"]["g_mac"]
+
+
+# ----------------------------------------------------------------------------- conv
+
+def gpu_conv(x_f32, w_f32, f, stride=1, pad=1, relu=0):
+    """float32 NHWC x and KhKwCinCout w -> quantise+pack on GPU -> conv -> unpack words."""
+    H = hobf()
+    n, h, w, cin = x_f32.shape
+    kh, kw, _, cout = w_f32.shape
+    xp = H.quantize_pack(f.we, f.wf, torch.from_numpy(x_f32.reshape(-1, cin)).cuda(), f.round)
+    wp = H.quantize_pack(f.we, f.wf, torch.from_numpy(w_f32.reshape(-1, cout)).cuda(), f.round)
+    yp = H.conv2d(f, xp, n, h, w, cin, wp, kh, kw, cout, stride, pad, relu)
+    ho, wo = H.conv_out_hw(h, w, kh, kw, stride, pad)
+    y = to_np_words(H.unpack(f.we, f.wfo, yp, n * ho * wo, cout)).reshape(n, ho, wo, cout)
+    return y
+
+
+def oracle_conv(x_f32, w_f32, f, stride=1, pad=1, relu=0):
+    xq = oracle.encode_f32(x_f32, f.we, f.wf, f.round)
+    wq = oracle.encode_f32(w_f32, f.we, f.wf, f.round)
+    return oracle.conv2d(xq, wq, f.we, f.wf, f.wfo, f.round, stride, pad, relu)
+
+
+def test_conv_C1_full():
+    """configs[0] in full, both ReLU settings, both rounding modes."""
+    H = hobf()
+    cfg = inputs.CONFIGS["C1"]
+    x, w = inputs.draw(cfg)
+    for rnd in (0, 1):
+        f = H.Fmt(5, 10, rnd)
+        for relu in (0, 1):
+            got = gpu_conv(x, w, f, relu=relu)
+            exp = oracle_conv(x, w, f, relu=relu)
+            assert np.array_equal(got, exp), (rnd, relu, np.argwhere(got != exp)[:5])
+
+
+@pytest.mark.parametrize("shape", [
+    # n, h, w, cin, cout, kh, kw, stride, pad
+    (2, 9, 7, 40, 50, 3, 3, 1, 1),     # ragged cin and cout, several tiles
+    (1, 5, 6, 33, 64, 3, 3, 2, 0),     # stride 2, no padding
+    (3, 4, 4, 1, 1, 3, 3, 1, 1),       # single channel in/out
+    (1, 6, 5, 8, 96, 1, 1, 1, 0),      # 1x1 kernel
+    (1, 7, 7, 5, 32, 5, 5, 1, 2),      # 5x5 kernel
+    (1, 1, 1, 16, 32, 3, 3, 1, 1),     # 1x1 image: every tap but the centre is padding
+])
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 3), (5, 10), (6, 7)])
+def test_conv_small_shapes(shape, we, wf):
+    H = hobf()
+    n, h, w, cin, cout, kh, kw, stride, pad = shape
+    x, wt = inputs.small_case(sum(shape) + we + wf, n, h, w, cin, cout, "normal", 0.5, kh, kw)
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd)
+        relu = rnd  # alternate
+        got = gpu_conv(x, wt, f, stride, pad, relu)
+        exp = oracle_conv(x, wt, f, stride, pad, relu)
+        assert np.array_equal(got, exp), np.argwhere(got != exp)[:5]
+
+
+def test_conv_specials_propagate():
+    """inf / NaN / overflow inputs: 0*inf = NaN through padding taps, inf + -inf = NaN."""
+    H = hobf()
+    f = H.Fmt(5, 3, 0)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((1, 5, 5, 8)).astype(np.float32)
+    w = rng.standard_normal((3, 3, 8, 32)).astype(np.float32)
+    x[0, 2, 2, 3] = np.inf
+    x[0, 0, 0, 1] = np.nan
+    x[0, 4, 4, 2] = 6e4       # near e5m3 max: products overflow
+    w[1, 1, 0, :] = np.inf
+    w[0, 2, 5, 7] = -np.inf
+    w[2, 2, 6, :] = 3e4
+    for relu in (0, 1):
+        got = gpu_conv(x, w, f, relu=relu)
+        exp = oracle_conv(x, w, f, relu=relu)
+        assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_conv_configs_sampled(name):
+    """Full-size configs in the bench launch configuration, checked on sampled
+    outputs the oracle computes one by one."""
+    H = hobf()
+    cfg = inputs.CONFIGS[name]
+    x, w = inputs.draw(cfg)
+    we, wf = cfg.formats[0]
+    f = H.Fmt(we, wf, 0)
+    got = gpu_conv(x, w, f)
+    xq = oracle.encode_f32(x, we, wf, 0)
+    wq = oracle.encode_f32(w, we, wf, 0)
+    rng = np.random.default_rng(5)
+    total = got.size
+    idx = np.unique(np.concatenate([rng.integers(0, total, 3000), np.arange(0, 64), np.arange(total - 64, total)]))
+    exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wf + 1, 0)
+    assert np.array_equal(got.ravel()[idx], exp)
+
+
+def test_conv_C5_sweep_sampled():
+    H = hobf()
+    cfg = inputs.CONFIGS["C5"]
+    x, w = inputs.draw(cfg, n=8)  # batch prefix of the config's draw
+    rng = np.random.default_rng(6)
+    for (we, wf) in cfg.formats:
+        f = H.Fmt(we, wf, 0)
+        got = gpu_conv(x, w, f)
+        xq = oracle.encode_f32(x, we, wf, 0)
+        wq = oracle.encode_f32(w, we, wf, 0)
+        idx = rng.integers(0, got.size, 150)
+        exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wf + 1, 0)
+        assert np.array_equal(got.ravel()[idx], exp), (we, wf)
+
+
+def test_conv_public_api_float():
+    """hobf.Conv2d (quantise+pack -> conv -> unpack to float32) equals the oracle's values."""
+    H = hobf()
+    x, w = inputs.small_case(21, 2, 10, 11, 24, 40)
+    f = H.Fmt(5, 10, 0)
+    layer = H.Conv2d(torch.from_numpy(w).cuda(), f, relu=True)
+    y = layer(torch.from_numpy(x).cuda()).cpu().numpy()
+    exp = oracle.decode_f64(oracle_conv(x, w, f, relu=1), 5, 11)
+    assert np.array_equal(y.astype(np.float64), exp)
