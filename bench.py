@@ -1,0 +1,369 @@
+#!/usr/bin/env python3
+"""Benchmark of the HOBFLOPS hot path on B200: bitsliced custom-FP conv MACs/s.
+
+One step = the whole hot path over one batch: quantise+pack the
+float32 activations and weights into bit planes (a0+a1), the bitsliced conv
+(a3-a8: staging, broadcast, MUL and ADD circuits over the serial (c,kh,kw)
+chain, ReLU epilogue) and unpack the output planes to float32 (a9).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+Multi-GPU: one process per GPU under torchrun; every rank runs its own batch
+shard (weak scaling, no collective on the data path); timing is max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2007_06563_b200 import inputs  # noqa: E402  (no method arithmetic)
+
+METRIC = "bitsliced custom-FP conv MACs/s per format at 1/2/4/8 B200; % of LOP3 roofline"
+N_SM = 148
+LOP3_PER_SM_CLK = 64          # 4 SMSPs x 16 lanes/clk on the ALU pipe (B300_MICROARCH rt_SMSP=2; measured 63.7)
+SM_MAX_MHZ_FALLBACK = 1965.0  # B200_PROFILING.md clocks.max.sm
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hobf", choices=["hobf", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(inputs.CONFIGS))
+    ap.add_argument("--format", default=None, help="override format, e.g. e5m10")
+    ap.add_argument("--round", default="rne", choices=["rne", "rtz"])
+    ap.add_argument("--relu", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-macs", type=float, default=1.2e9,
+                    help="MACs of the bounded oracle sample (about 10 s on 16 host cores)")
+    return ap.parse_args(argv)
+
+
+def fmt_of(cfg, override):
+    if override:
+        we, wf = override[1:].split("m")
+        return int(we), int(wf)
+    return cfg.formats[0]
+
+
+# ----------------------------------------------------------------------------- distributed plumbing
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def done(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm (the oracle)
+
+def run_reference(a, dist):
+    """--impl reference: the CPU oracle, as it stands, on the host cores; rank 0 only."""
+    if dist.rank != 0:
+        return 0
+    import oracle  # test infrastructure: allowed in bench.py's reference / cpu_baseline legs
+    cfg = inputs.CONFIGS[a.config]
+    we, wf = fmt_of(cfg, a.format)
+    rnd = 0 if a.round == "rne" else 1
+    cores = os.cpu_count() or 1
+    x, w = inputs.draw(cfg, n=1)
+    per_img = cfg.macs(1)
+    # bounded sample per step: the conv of the first `rows` input rows of image 0
+    # (an image of height `rows`), sized so that K+W steps take a few minutes
+    rows = max(1, min(cfg.h, int(round(cfg.h * min(1.0, 0.4e9 / per_img)))))
+    xq = oracle.encode_f32(x, we, wf, rnd)
+    wq = oracle.encode_f32(w, we, wf, rnd)
+    xin = np.ascontiguousarray(xq[:, :rows])
+    ho_s = (rows + 2 * cfg.pad - cfg.kh) // cfg.stride + 1
+    sample_macs = ho_s * cfg.wo * cfg.cout * cfg.cin * cfg.kh * cfg.kw
+
+    def step():
+        y = oracle.conv2d(xin, wq, we, wf, wf + 1, rnd, cfg.stride, cfg.pad, a.relu, nthreads=cores)
+        return y
+
+    for _ in range(a.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = sample_macs * a.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MAC/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": f"e{we}m{wf}-exact-scalar", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.text}", "format": f"e{we}m{wf}", "round": a.round,
+                   "batch": 1, "sample_output_rows": rows},
+        "cpu_baseline": {"value": value, "unit": "MAC/s", "cores": cores, "kind": "oracle",
+                         "sample": f"conv of the first {rows} of {cfg.h} input rows of image 0 of {cfg.name} per step"},
+        "e2e": {"value": value, "unit": "MAC/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(cfg, we, wf, rnd, relu, target_macs):
+    import oracle
+    cores = os.cpu_count() or 1
+    per_img = cfg.macs(1)
+    n = max(1, min(cfg.n, int(round(target_macs / per_img))))
+    x, w = inputs.draw(cfg, n=n)
+    xq = oracle.encode_f32(x, we, wf, rnd)
+    wq = oracle.encode_f32(w, we, wf, rnd)
+    t0 = time.perf_counter()
+    oracle.conv2d(xq, wq, we, wf, wf + 1, rnd, cfg.stride, cfg.pad, relu, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": cfg.macs(n) / dt, "unit": "MAC/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} of {cfg.n} images of {cfg.name} (full conv, every output exact), {dt:.1f} s"}
+
+
+def parity_sample(cfg, we, wf, rnd, relu, y_words, x_f32, w_f32, k=256):
+    import oracle
+    xq = oracle.encode_f32(x_f32, we, wf, rnd)
+    wq = oracle.encode_f32(w_f32, we, wf, rnd)
+    rng = np.random.default_rng(123)
+    idx = rng.integers(0, y_words.size, k)
+    exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wf + 1, rnd, cfg.stride, cfg.pad, relu)
+    return {"checked": int(k), "mismatches": int((y_words.ravel()[idx] != exp).sum())}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def run_gpu(a, dist):
+    import torch
+    from paper_2007_06563_b200 import hobf as H
+
+    torch.cuda.set_device(dist.local)
+    dev = torch.device("cuda", dist.local)
+    cfg = inputs.CONFIGS[a.config]
+    we, wf = fmt_of(cfg, a.format)
+    rnd = 0 if a.round == "rne" else 1
+    f = H.Fmt(we, wf, rnd)
+    n = cfg.n
+    x_np, w_np = inputs.draw(cfg, n=n, shard=dist.rank)
+    rows_x, rows_w, rows_y = n * cfg.h * cfg.w, cfg.kh * cfg.kw * cfg.cin, n * cfg.ho * cfg.wo
+    x = torch.from_numpy(x_np.reshape(rows_x, cfg.cin)).to(dev)
+    wt = torch.from_numpy(w_np.reshape(rows_w, cfg.cout)).to(dev)
+    xp = torch.empty(H.planes_shape(rows_x, cfg.cin, f.nin), dtype=torch.int32, device=dev)
+    wp = torch.empty(H.planes_shape(rows_w, cfg.cout, f.nin), dtype=torch.int32, device=dev)
+    yp = torch.empty(H.planes_shape(rows_y, cfg.cout, f.nout), dtype=torch.int32, device=dev)
+    y = torch.empty((rows_y, cfg.cout), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+    launches = [0]
+
+    def step(conv_ev=None):
+        H.quantize_pack(we, wf, x, rnd, out=xp, stream=stream); launches[0] += H.last_launch_count()
+        H.quantize_pack(we, wf, wt, rnd, out=wp, stream=stream); launches[0] += H.last_launch_count()
+        if conv_ev:
+            conv_ev[0].record(stream)
+        H.conv2d(f, xp, n, cfg.h, cfg.w, cfg.cin, wp, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad, a.relu,
+                 out=yp, stream=stream); launches[0] += H.last_launch_count()
+        if conv_ev:
+            conv_ev[1].record(stream)
+        H.unpack_f32(we, f.wfo, yp, rows_y, cfg.cout, out=y, stream=stream); launches[0] += H.last_launch_count()
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    K = a.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = ClockSampler(torch.cuda.current_device())
+    launches[0] = 0
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.15)
+    for k in range(K):
+        flush.fill_(k)                      # evict L2 between timed steps (untimed)
+        ev[k][0].record(stream)
+        step(cev[k])
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dist.barrier()
+    step_ms = sum(s.elapsed_time(e) for s, e in ev)
+    conv_ms = sum(s.elapsed_time(e) for s, e in cev)
+    gpu_launches = launches[0]
+    t_max = dist.max(step_ms) / 1e3
+    conv_max = dist.max(conv_ms) / 1e3
+    macs_rank = cfg.macs(n)
+    value = dist.world * macs_rank * K / t_max
+
+    # --- e2e through the public API with host buffers: pinned h2d of x, step, d2h of y
+    e2e = None
+    if not a.no_e2e:
+        xh = torch.from_numpy(x_np.reshape(rows_x, cfg.cin)).pin_memory()
+        yh = torch.empty((rows_y, cfg.cout), dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            x.copy_(xh, non_blocking=True); step(); yh.copy_(y, non_blocking=True)
+        torch.cuda.synchronize()
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        dist.barrier()
+        for k in range(K):
+            flush.fill_(k)
+            eev[k][0].record(stream)
+            x.copy_(xh, non_blocking=True)
+            step()
+            yh.copy_(y, non_blocking=True)
+            eev[k][1].record(stream)
+        torch.cuda.synchronize()
+        e2e_s = dist.max(sum(s.elapsed_time(e) for s, e in eev) / 1e3)
+        e2e = {"value": dist.world * macs_rank * K / e2e_s, "unit": "MAC/s",
+               "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(yh.numel() * 4)}
+
+    # --- roofline of the dominant kernel (conv): algorithmic lop3 = MACs * G / 32
+    g = H.gate_count(f)
+    lop3_per_launch = macs_rank * g["mac"] / 32.0
+    sm_mhz = clk["sm_max_mhz"] or SM_MAX_MHZ_FALLBACK
+    peak = N_SM * LOP3_PER_SM_CLK * sm_mhz * 1e6
+    achieved = lop3_per_launch * K / conv_max
+    sink = torch.zeros(1024, dtype=torch.int32, device=dev)
+    H.lop3_peak(N_SM * 4, 256, 200, sink)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    nops = H.lop3_peak(N_SM * 4, 256, 2000, sink)
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    measured_peak = nops / (pe0.elapsed_time(pe1) / 1e3)
+
+    if dist.rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "MAC/s", "n_gpus": dist.world, "steps": K, "warmup": a.warmup,
+        "ms_per_step": t_max / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": f"e{we}m{wf}->e{we}m{wf + 1} custom FP, bitsliced u32 lop3", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.text}", "format": f"e{we}m{wf}", "round": a.round,
+                   "relu": a.relu, "global_batch": n * dist.world, "per_gpu_batch": n,
+                   "dense_macs_per_step": macs_rank * dist.world, "l2": "flushed (256 MiB write) between timed steps",
+                   "step": "quantize_pack(x) + quantize_pack(w) + conv2d + unpack_f32(y)",
+                   "parallelism": f"dp{dist.world} (batch shards, no collective)"},
+        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlop3/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "conv2d", "gates_per_32lane_mac": g["mac"],
+                     "peak_source": f"derived: {N_SM} SM x {LOP3_PER_SM_CLK} lop3/clk x {sm_mhz:.0f} MHz",
+                     "measured_lop3_peak": measured_peak / 1e12,
+                     "conv_ms_per_step": conv_max / K * 1e3,
+                     "mac_per_s_conv_only": dist.world * macs_rank * K / conv_max,
+                     "paper_G257_roof_frac": (macs_rank * K / conv_max) / (peak * 32 / 257)},
+        "e2e": e2e,
+        "gpu_launches": gpu_launches,
+        "clocks": clk,
+    }
+    if dist.world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, we, wf, rnd, a.relu, a.cpu_sample_macs)
+        yw = H.unpack(we, f.wfo, yp, rows_y, cfg.cout).cpu().numpy().view(np.uint32)
+        line["parity_sample"] = parity_sample(cfg, we, wf, rnd, a.relu, yw, x_np, w_np)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    a = parse_args(argv)
+    dist = Dist()
+    if a.impl == "reference":
+        rc = run_reference(a, dist)
+        return rc
+    import torch
+    dist.init("nccl" if torch.cuda.is_available() else "gloo")
+    try:
+        return run_gpu(a, dist)
+    finally:
+        dist.done()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -289,6 +289,7 @@ hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
   a.variant = 0;
+  a.one = 1;
   if (e->conv(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;

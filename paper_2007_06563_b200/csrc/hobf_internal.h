@@ -12,6 +12,7 @@ struct ConvArgs {
   int n, h, w, cin, kh, kw, cout, stride, pad, relu, ho, wo;
   int64_t items;       // n * ho * wo * ceil(cout/32)
   int variant;         // kernel variant (0 = auto)
+  int one;             // always 1 (opaque to the compiler, see bcast_bit)
 };
 
 typedef cudaError_t (*conv_launcher)(const ConvArgs&, cudaStream_t);

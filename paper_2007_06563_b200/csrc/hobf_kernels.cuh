@@ -16,6 +16,24 @@
 
 namespace hobf {
 
+// Broadcast bit b of w to all 32 lanes (0 or ~0) without touching the ALU
+// pipe, which the lop3 gates saturate: (w * 2^(31-b)) puts bit b in the sign
+// position (IMAD), and the high word of (that * one) as a signed 64-bit
+// product is its sign extension (IMAD.HI).  `one` is a runtime 1 so that
+// ptxas cannot turn the IMAD.HI into an ALU shift.
+// 2^(31-b) for b = 0..31, read from constant memory so that the multiply
+// stays an IMAD (a visible power of two would become an ALU shift).
+__constant__ uint32_t c_lift[32] = {
+    1u << 31, 1u << 30, 1u << 29, 1u << 28, 1u << 27, 1u << 26, 1u << 25, 1u << 24,
+    1u << 23, 1u << 22, 1u << 21, 1u << 20, 1u << 19, 1u << 18, 1u << 17, 1u << 16,
+    1u << 15, 1u << 14, 1u << 13, 1u << 12, 1u << 11, 1u << 10, 1u << 9,  1u << 8,
+    1u << 7,  1u << 6,  1u << 5,  1u << 4,  1u << 3,  1u << 2,  1u << 1,  1u << 0};
+
+__device__ __forceinline__ uint32_t bcast_bit(uint32_t w, uint32_t lift, int32_t one) {
+  const int32_t t = (int32_t)(w * lift);
+  return (uint32_t)__mulhi(t, one);
+}
+
 // ---------------------------------------------------------------------------
 // conv2d: one thread = one output pixel x one group of 32 output channels.
 // Lanes of every register are the 32 output channels (the paper's tiling of
@@ -45,6 +63,7 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
 #pragma unroll 1
   for (int c = 0; c < a.cin; c++) {
     const int cg = c >> 5, b = c & 31;
+    const uint32_t lift = c_lift[b];  // bit b -> bit 31 (multiply on the FMA pipe)
 #pragma unroll 1
     for (int kh = 0; kh < a.kh; kh++) {
       const int iy = oy * a.stride - a.pad + kh;
@@ -60,7 +79,7 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
             X[4 * q + 0] = v.x; X[4 * q + 1] = v.y; X[4 * q + 2] = v.z; X[4 * q + 3] = v.w;
           }
 #pragma unroll
-          for (int j = 0; j < F::NPI; j++) X[j] = 0u - ((X[j] >> b) & 1u);  // broadcast
+          for (int j = 0; j < F::NPI; j++) X[j] = bcast_bit(X[j], lift, a.one);  // broadcast
         } else {
 #pragma unroll
           for (int j = 0; j < F::NPI; j++) X[j] = 0u;  // zero padding = +0 (L11, L14)
