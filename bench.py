@@ -46,6 +46,9 @@ def parse_args(argv=None):
     ap.add_argument("--format", default=None, help="override format, e.g. e5m10")
     ap.add_argument("--round", default="rne", choices=["rne", "rtz"])
     ap.add_argument("--relu", type=int, default=0)
+    ap.add_argument("--kernel", default="auto", choices=["auto", "gates", "tables"],
+                    help="conv kernel: gates = full lop3 MAC (hobf_conv2d); tables = prepared weights "
+                         "(hobf_prepare_weights + hobf_conv2d_prepared); auto = tables when the format has them")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-macs", type=float, default=1.2e9,
@@ -239,6 +242,11 @@ def run_gpu(a, dist):
     wp = torch.empty(H.planes_shape(rows_w, cfg.cout, f.nin), dtype=torch.int32, device=dev)
     yp = torch.empty(H.planes_shape(rows_y, cfg.cout, f.nout), dtype=torch.int32, device=dev)
     y = torch.empty((rows_y, cfg.cout), dtype=torch.float32, device=dev)
+    tab_words = H.wtab_words(f, cfg.kh, cfg.kw, cfg.cin, cfg.cout)
+    use_tab = a.kernel == "tables" or (a.kernel == "auto" and tab_words > 0)
+    wtab = torch.empty(max(tab_words, 4), dtype=torch.int32, device=dev) if use_tab else None
+    xrec = (torch.empty(max(H.xrec_words(n, cfg.h, cfg.w, cfg.cin, cfg.pad), 4), dtype=torch.int32, device=dev)
+            if use_tab else None)
     stream = torch.cuda.current_stream()
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
     launches = [0]
@@ -246,10 +254,20 @@ def run_gpu(a, dist):
     def step(conv_ev=None):
         H.quantize_pack(we, wf, x, rnd, out=xp, stream=stream); launches[0] += H.last_launch_count()
         H.quantize_pack(we, wf, wt, rnd, out=wp, stream=stream); launches[0] += H.last_launch_count()
+        if use_tab:
+            H.prepare_weights(f, wp, cfg.kh, cfg.kw, cfg.cin, cfg.cout, out=wtab, stream=stream)
+            launches[0] += H.last_launch_count()
+            H.prepare_activations(f, xp, n, cfg.h, cfg.w, cfg.cin, cfg.pad, out=xrec, stream=stream)
+            launches[0] += H.last_launch_count()
         if conv_ev:
             conv_ev[0].record(stream)
-        H.conv2d(f, xp, n, cfg.h, cfg.w, cfg.cin, wp, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad, a.relu,
-                 out=yp, stream=stream); launches[0] += H.last_launch_count()
+        if use_tab:
+            H.conv2d_prepared(f, xrec, n, cfg.h, cfg.w, cfg.cin, wtab, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad,
+                              a.relu, out=yp, stream=stream)
+        else:
+            H.conv2d(f, xp, n, cfg.h, cfg.w, cfg.cin, wp, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad, a.relu,
+                     out=yp, stream=stream)
+        launches[0] += H.last_launch_count()
         if conv_ev:
             conv_ev[1].record(stream)
         H.unpack_f32(we, f.wfo, yp, rows_y, cfg.cout, out=y, stream=stream); launches[0] += H.last_launch_count()
@@ -307,7 +325,8 @@ def run_gpu(a, dist):
 
     # --- roofline of the dominant kernel (conv): algorithmic lop3 = MACs * G / 32
     g = H.gate_count(f)
-    lop3_per_launch = macs_rank * g["mac"] / 32.0
+    G = g["mac_tab"] if use_tab else g["mac"]
+    lop3_per_launch = macs_rank * G / 32.0
     sm_mhz = clk["sm_max_mhz"] or SM_MAX_MHZ_FALLBACK
     peak = N_SM * LOP3_PER_SM_CLK * sm_mhz * 1e6
     achieved = lop3_per_launch * K / conv_max
@@ -329,11 +348,13 @@ def run_gpu(a, dist):
         "config": {"workload": f"{cfg.name}: {cfg.text}", "format": f"e{we}m{wf}", "round": a.round,
                    "relu": a.relu, "global_batch": n * dist.world, "per_gpu_batch": n,
                    "dense_macs_per_step": macs_rank * dist.world, "l2": "flushed (256 MiB write) between timed steps",
-                   "step": "quantize_pack(x) + quantize_pack(w) + conv2d + unpack_f32(y)",
+                   "step": ("quantize_pack(x) + quantize_pack(w) + prepare_weights + prepare_activations + conv2d_prepared + unpack_f32(y)"
+                            if use_tab else "quantize_pack(x) + quantize_pack(w) + conv2d + unpack_f32(y)"),
                    "parallelism": f"dp{dist.world} (batch shards, no collective)"},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlop3/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "conv2d", "gates_per_32lane_mac": g["mac"],
+                     "kernel": "conv2d_prepared (weight tables)" if use_tab else "conv2d (full lop3 MAC)",
+                     "gates_per_32lane_mac": G, "gates_full_mac": g["mac"],
                      "peak_source": f"derived: {N_SM} SM x {LOP3_PER_SM_CLK} lop3/clk x {sm_mhz:.0f} MHz",
                      "measured_lop3_peak": measured_peak / 1e12,
                      "conv_ms_per_step": conv_max / K * 1e3,

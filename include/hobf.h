@@ -106,9 +106,46 @@ hobf_status hobf_mac_planes(hobf_fmt f, uint32_t* d_acc, const uint32_t* d_a, co
                             int64_t n_groups, hobf_stream stream);
 
 /* Gate counts of the generated circuits (lop3 per 32 lanes; P:249 analogue):
- * mac = multiplier and adder mapped jointly (the conv inner loop body). Any
- * output pointer may be NULL. */
-hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add, int32_t* relu);
+ * mac = multiplier and adder mapped jointly (the hobf_conv2d inner loop body);
+ * mac_tab = the hobf_conv2d_prepared inner loop body (multiplier significand
+ * read from the weight table).  Any output pointer may be NULL. */
+hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add, int32_t* relu,
+                            int32_t* mac_tab);
+
+/* Prepared weights ("kernel data pre-transformed").  In the paper's
+ * tiling the 32 lanes of a register are 32 output channels and the activation
+ * is broadcast across them, so inside the conv the activation is
+ * one scalar per thread: for every weight the library precomputes, per lane,
+ * the rounded significand product with each possible activation fraction
+ * (plus the exception algebra for x = 0 / inf / NaN) once, and the conv reads
+ * the row the activation selects instead of evaluating the multiplier array.
+ * Results are identical to hobf_conv2d.
+ *
+ * hobf_wtab_words: size in uint32 words of the table buffer for these weights,
+ * or -1 if the format has no table kernel (wf > 7, extended class).
+ * Layout: [kh][kw][cin][ceil(cout/32)][2^wf + 3 rows][roundup(wf + we + 6, 4) planes]. */
+int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t cout);
+
+/* Build the weight table from weight planes (layout as for hobf_conv2d). */
+hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cin,
+                                 int32_t cout, uint32_t* d_wtab, hobf_stream stream);
+
+/* Prepared activations: because the activation is broadcast (one scalar per
+ * thread), the conv reads it per element, not bitsliced.  Records are one
+ * uint32 per element, zero-padded by `pad` on each spatial side, layout
+ * [n][cin][h+2pad][w+2pad]: the canonical F(we,wf) word in bits [0,20) and the
+ * weight-table row it selects in bits [20,32).  Formats as for
+ * hobf_wtab_words.  hobf_xrec_words returns the buffer size in words. */
+int64_t hobf_xrec_words(int32_t n, int32_t h, int32_t w, int32_t cin, int32_t pad);
+hobf_status hobf_prepare_activations(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w,
+                                     int32_t cin, int32_t pad, uint32_t* d_xrec, hobf_stream stream);
+
+/* hobf_conv2d on prepared activations (built with the same pad) and prepared
+ * weights; identical results.  Output planes as for hobf_conv2d. */
+hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
+                                 int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout,
+                                 int32_t stride, int32_t pad, int32_t relu, uint32_t* d_y_planes,
+                                 hobf_stream stream);
 
 /* LOP3 issue-rate microbenchmark (roofline denominator): launches `blocks` x
  * `threads` threads, each issuing `iters` x 128 dependent-free lop3 ops;

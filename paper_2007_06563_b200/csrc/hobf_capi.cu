@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "../../include/hobf.h"
 #include "hobf_internal.h"
@@ -16,9 +17,10 @@ using hobf::FormatEntry;
 #define HOBF_DECLARE(TAG)                                                                    \
   cudaError_t hobf_launch_conv_##TAG(const hobf::ConvArgs& a, cudaStream_t s);               \
   cudaError_t hobf_launch_mac_##TAG(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n, \
-                                    cudaStream_t s);
-#define HOBF_ENTRY(TAG, WE, WF, RND, GM, GMUL, GADD, GRELU) \
-  {WE, WF, RND, GM, GMUL, GADD, GRELU, hobf_launch_conv_##TAG, hobf_launch_mac_##TAG},
+                                    cudaStream_t s);                                         \
+  cudaError_t hobf_launch_convtab_##TAG(const hobf::ConvArgs& a, cudaStream_t s);
+#define HOBF_ENTRY(TAG, WE, WF, RND, GM, GMUL, GADD, GRELU, GTAB) \
+  {WE, WF, RND, GM, GMUL, GADD, GRELU, GTAB, hobf_launch_conv_##TAG, hobf_launch_mac_##TAG, hobf_launch_convtab_##TAG},
 #include "gen/hobf_table.inc"
 
 static const FormatEntry kFormats[] = {HOBF_TABLE_ENTRIES};
@@ -156,6 +158,131 @@ static unsigned warp_grid(int64_t items) {
   return (unsigned)blocks;
 }
 
+// ----------------------------------------------------------------------------- weight tables
+// Largest wF with a prepared-weights (table) kernel; the table has 2^wF + 3 rows.
+static const int kTabMaxWf = 7;
+
+__host__ __device__ static inline int tab_width(int we, int wf) { return (wf + 1) + (we + 2) + 3; }
+__host__ __device__ static inline int tab_rows(int wf) { return (1 << wf) + 3; }
+
+// One table entry for weight word w (canonical) and table row r (see
+// conv_tab_kernel / gen/fpgen.product_from_table):
+//   bits [0, wF+1)         rounded product fraction (round to wF+1 bits at the
+//                          product's own binade, RNE ties-to-even or RTZ)
+//   bits [wF+1, wF+wE+3)   Epart = eb - bias + (normalise carry + round carry),
+//                          wE+2-bit two's complement; the conv adds ea
+//   bit  wF+wE+3           weight sign (the conv XORs the activation sign)
+//   bits wF+wE+4, +5       product class K0, K1 (00 zero, 01 normal, 10 inf,
+//                          11 NaN), exception algebra of S:68 / SURVEY 8(c) mul
+// Rows: r < 2^wF: normal x with fraction r; 2^wF: x zero; +1: x inf; +2: x NaN.
+__device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int rnd) {
+  const int wfo = wf + 1, EW = we + 2;
+  const uint32_t exc = (w >> (wf + we + 1)) & 3u;
+  const uint32_t sw = (w >> (wf + we)) & 1u;
+  const uint32_t eb = (w >> wf) & ((1u << we) - 1u);
+  const uint32_t fb = w & ((1u << wf) - 1u);
+  const int sbit = wfo + EW, k0 = sbit + 1, k1 = sbit + 2;
+  const uint32_t NAN_E = (1u << k0) | (1u << k1);
+  const uint32_t INF_E = (1u << k1) | (sw << sbit);
+  const uint32_t ZERO_E = sw << sbit;
+  const int nrows = 1 << wf;
+  if (r == nrows) return (exc & 2u) ? NAN_E : ZERO_E;                  // x = 0: 0*inf, 0*NaN = NaN
+  if (r == nrows + 1) return (exc == 0u || exc == 3u) ? NAN_E : INF_E;  // x = inf: inf*0 = NaN
+  if (r == nrows + 2) return NAN_E;                                    // x = NaN
+  if (exc == 0u) return ZERO_E;
+  if (exc == 2u) return INF_E;
+  if (exc == 3u) return NAN_E;
+  // both normal: exact significand product, normalise, round to wfo bits
+  const uint32_t ma = (1u << wf) | (uint32_t)r, mb = (1u << wf) | fb;
+  const uint32_t P = ma * mb;  // < 2^(2wf+2) <= 2^16 for wf <= 7
+  const uint32_t top = (P >> (2 * wf + 1)) & 1u;
+  const uint32_t N = top ? P : (P << 1);       // leading one at bit 2wf+1
+  uint32_t kept = N >> wf;                     // wfo+1 bits
+  const uint32_t rem = N & ((1u << wf) - 1u);  // below the kept bits
+  const uint32_t half = 1u << (wf - 1);
+  if (rnd == 0 && (rem > half || (rem == half && (kept & 1u)))) kept += 1u;
+  uint32_t inc = top;
+  if (kept == (2u << wfo)) { kept >>= 1; inc += 1u; }
+  const uint32_t frac = kept - (1u << wfo);
+  const int bias = (1 << (we - 1)) - 1;
+  const uint32_t ep = (uint32_t)((int)eb - bias + (int)inc) & ((1u << EW) - 1u);
+  return frac | (ep << wfo) | (sw << sbit) | (1u << k0);
+}
+
+// Activation records for hobf_conv2d_prepared: one uint32 per element in a
+// zero-padded [n][c][h+2p][w+2p] layout: the canonical x word in bits [0, 20)
+// and the weight-table row it selects in bits [20, 32) (row = frac if normal,
+// 2^wF + 0/1/2 for zero/inf/NaN; padding = +0 -> row 2^wF).  One thread per
+// padded pixel, looping over the channels; consecutive threads write
+// consecutive columns (coalesced).
+__device__ __forceinline__ uint32_t xrec_of(uint32_t x, int we, int wf) {
+  const uint32_t exc = (x >> (wf + we + 1)) & 3u;
+  const uint32_t row = exc == 1u ? (x & ((1u << wf) - 1u)) : ((1u << wf) + (exc == 0u ? 0u : exc - 1u));
+  return x | (row << 20);
+}
+
+__global__ void __launch_bounds__(256) prepare_acts_kernel(const uint32_t* __restrict__ planes, int n, int h, int w,
+                                                           int cin, int pad, int we, int wf,
+                                                           uint32_t* __restrict__ rec) {
+  const int Hp = h + 2 * pad, Wp = w + 2 * pad;
+  const int64_t npix = (int64_t)n * Hp * Wp;
+  const int CG = (cin + 31) >> 5;
+  const int nb = 3 + we + wf, np = (nb + 3) / 4 * 4;
+  const uint32_t zero_rec = xrec_of(0u, we, wf);
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+    const int ixp = (int)(p % Wp);
+    const int iyp = (int)((p / Wp) % Hp);
+    const int ni = (int)(p / ((int64_t)Wp * Hp));
+    const int iy = iyp - pad, ix = ixp - pad;
+    const bool inside = iy >= 0 && iy < h && ix >= 0 && ix < w;
+    uint32_t* out = rec + ((int64_t)ni * cin * Hp + iyp) * Wp + ixp;
+    for (int cg = 0; cg < CG; cg++) {
+      uint32_t P[32];
+      if (inside) {
+        const uint32_t* src = planes + ((((int64_t)ni * h + iy) * w + ix) * CG + cg) * np;
+        for (int j = 0; j < nb; j++) P[j] = __ldg(src + j);
+      }
+      const int cmax = min(32, cin - cg * 32);
+      for (int b = 0; b < cmax; b++) {
+        uint32_t v = zero_rec;
+        if (inside) {
+          uint32_t x = 0u;
+          for (int j = 0; j < nb; j++) x |= ((P[j] >> b) & 1u) << j;
+          v = xrec_of(x, we, wf);
+        }
+        out[(int64_t)(cg * 32 + b) * Hp * Wp] = v;
+      }
+    }
+  }
+}
+
+// Warp per (weight row, output-channel group, table row): each lane decodes
+// its weight from the planes (shfl transpose), computes its entry, and the
+// entry bits are ballot-transposed back into NPT planes.
+__global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restrict__ wplanes, int64_t wrows, int G,
+                                                         int we, int wf, int rnd, uint32_t* __restrict__ wtab) {
+  const int lane = threadIdx.x & 31;
+  const int npi = (3 + we + wf + 3) / 4 * 4;
+  const int rows = tab_rows(wf);
+  const int npt = (tab_width(we, wf) + 3) / 4 * 4;
+  const int64_t items = wrows * G * rows;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    const int r = (int)(it % rows);
+    const int64_t grp = it / rows;  // (weight row, group)
+    const uint32_t mine = lane < npi ? __ldg(wplanes + grp * npi + lane) : 0u;
+    uint32_t w = 0u;
+    for (int j = 0; j < 3 + we + wf; j++) w |= ((__shfl_sync(0xffffffffu, mine, j) >> lane) & 1u) << j;
+    const uint32_t e = tab_entry(w, r, we, wf, rnd);
+    uint32_t out = 0u;
+    for (int j = 0; j < npt; j++) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (e >> j) & 1u);
+      if (lane == j) out = bal;
+    }
+    if (lane < npt) wtab[it * npt + lane] = out;
+  }
+}
+
 // ----------------------------------------------------------------------------- lop3 peak
 __global__ void lop3_peak_kernel(uint32_t* sink, uint32_t seed, int iters) {
   uint32_t v[8];
@@ -290,6 +417,7 @@ hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
   a.variant = 0;
   a.one = 1;
+  a.two = 2u;
   if (e->conv(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;
@@ -308,13 +436,110 @@ hobf_status hobf_mac_planes(hobf_fmt f, uint32_t* d_acc, const uint32_t* d_a, co
   return HOBF_OK;
 }
 
-hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add, int32_t* relu) {
+hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add, int32_t* relu,
+                            int32_t* mac_tab) {
   const FormatEntry* e = f.extended ? nullptr : find_format(f.we, f.wf, f.round);
   if (!e) return HOBF_EUNSUPPORTED;
   if (mac) *mac = e->g_mac;
   if (mul) *mul = e->g_mul;
   if (add) *add = e->g_add;
   if (relu) *relu = e->g_relu;
+  if (mac_tab) *mac_tab = e->g_tab;
+  return HOBF_OK;
+}
+
+// Kernel variant of hobf_conv2d_prepared (see launch_conv_tab); HOBF_CONV_VARIANT overrides.
+static int conv_tab_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HOBF_CONV_VARIANT");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
+static const FormatEntry* tab_format(hobf_fmt f) {
+  if (f.extended || f.wf > kTabMaxWf) return nullptr;
+  return find_format(f.we, f.wf, f.round);
+}
+
+int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t cout) {
+  if (!fmt_ok(f.we, f.wf) || kh <= 0 || kw <= 0 || cin <= 0 || cout <= 0) return -1;
+  if (!tab_format(f)) return -1;
+  const int64_t npt = (tab_width(f.we, f.wf) + 3) / 4 * 4;
+  return (int64_t)kh * kw * cin * ((cout + 31) / 32) * tab_rows(f.wf) * npt;
+}
+
+hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cin,
+                                 int32_t cout, uint32_t* d_wtab, hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || kh < 0 || kw < 0 || cin < 0 || cout < 0)
+    return HOBF_EINVAL;
+  if (kh == 0 || kw == 0 || cin == 0 || cout == 0) return HOBF_ESHAPE;
+  if (!tab_format(f)) return HOBF_EUNSUPPORTED;
+  if (!d_w_planes || !d_wtab || !aligned16(d_w_planes) || !aligned16(d_wtab)) return HOBF_EINVAL;
+  const int G = (cout + 31) / 32;
+  const int64_t wrows = (int64_t)kh * kw * cin;
+  const int64_t items = wrows * G * tab_rows(f.wf);
+  build_wtab_kernel<<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(d_w_planes, wrows, G, f.we, f.wf, f.round,
+                                                                          d_wtab);
+  if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+int64_t hobf_xrec_words(int32_t n, int32_t h, int32_t w, int32_t cin, int32_t pad) {
+  if (n < 0 || h <= 0 || w <= 0 || cin <= 0 || pad < 0) return -1;
+  return (int64_t)n * cin * (h + 2 * pad) * (w + 2 * pad);
+}
+
+hobf_status hobf_prepare_activations(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w,
+                                     int32_t cin, int32_t pad, uint32_t* d_xrec, hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(f.we, f.wf) || n < 0 || h < 0 || w < 0 || cin < 0 || pad < 0) return HOBF_EINVAL;
+  if (h == 0 || w == 0 || cin == 0) return HOBF_ESHAPE;
+  if (!tab_format(f)) return HOBF_EUNSUPPORTED;
+  if (n == 0) return HOBF_OK;
+  if (!d_x_planes || !d_xrec || !aligned16(d_x_planes)) return HOBF_EINVAL;
+  const int64_t npix = (int64_t)n * (h + 2 * pad) * (w + 2 * pad);
+  int64_t blocks = (npix + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  prepare_acts_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_x_planes, n, h, w, cin, pad, f.we, f.wf,
+                                                                            d_xrec);
+  if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                 const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
+                                 int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
+  const uint32_t* d_x_planes = d_xrec;
+  g_last_launches = 0;
+  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
+    return HOBF_EINVAL;
+  if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)
+    return HOBF_EINVAL;
+  if (h == 0 || w == 0 || cin == 0 || kh == 0 || kw == 0 || cout == 0) return HOBF_ESHAPE;
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
+  const FormatEntry* e = tab_format(f);
+  if (!e) return HOBF_EUNSUPPORTED;
+  if (n == 0) return HOBF_OK;
+  if (!d_x_planes || !d_wtab || !d_y_planes) return HOBF_EINVAL;
+  if (!aligned16(d_x_planes) || !aligned16(d_wtab) || !aligned16(d_y_planes)) return HOBF_EINVAL;
+  ConvArgs a;
+  a.x = d_x_planes; a.wt = d_wtab; a.y = d_y_planes;
+  a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
+  a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
+  a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
+  a.variant = conv_tab_variant();
+  a.row_mul = 1u << 12;
+  for (int j = 0; j < 32; j++) a.lift[j] = 1u << (31 - j);
+  a.one = 1;
+  a.two = 2u;
+  if (e->conv_tab(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
   return HOBF_OK;
 }
 

@@ -7,21 +7,25 @@ namespace hobf {
 
 struct ConvArgs {
   const uint32_t* x;   // input planes  [n][h][w][ceil(cin/32)][NPI]
-  const uint32_t* wt;  // weight planes [kh][kw][cin][ceil(cout/32)][NPI]
+  const uint32_t* wt;  // weight planes [kh][kw][cin][ceil(cout/32)][NPI], or weight tables
   uint32_t* y;         // output planes [n][ho][wo][ceil(cout/32)][NPO]
   int n, h, w, cin, kh, kw, cout, stride, pad, relu, ho, wo;
   int64_t items;       // n * ho * wo * ceil(cout/32)
   int variant;         // kernel variant (0 = auto)
   int one;             // always 1 (opaque to the compiler, see bcast_bit)
+  unsigned two;        // always 2 (see bit01)
+  unsigned row_mul;    // 2^12: IMAD.HI(rec, row_mul) = rec >> 20 (table row of an activation record)
+  unsigned lift[32];   // lift[j] = 2^(31-j), runtime values so the multiplies stay IMADs
 };
 
 typedef cudaError_t (*conv_launcher)(const ConvArgs&, cudaStream_t);
 typedef cudaError_t (*mac_launcher)(uint32_t*, const uint32_t*, const uint32_t*, int64_t, cudaStream_t);
 
 struct FormatEntry {
-  int we, wf, rnd, g_mac, g_mul, g_add, g_relu;
+  int we, wf, rnd, g_mac, g_mul, g_add, g_relu, g_tab;
   conv_launcher conv;
   mac_launcher mac;
+  conv_launcher conv_tab;  // conv with the multiplier read from per-weight tables
 };
 
 }  // namespace hobf

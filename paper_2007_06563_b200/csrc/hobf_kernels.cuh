@@ -34,6 +34,22 @@ __device__ __forceinline__ uint32_t bcast_bit(uint32_t w, uint32_t lift, int32_t
   return (uint32_t)__mulhi(t, one);
 }
 
+// (c, kh, kw) tap counter in the order of the reduction (c outermost, L10).
+struct TapIter {
+  int c = 0, kh = 0, kw = 0;
+  __device__ __forceinline__ void next(int KH, int KW) {
+    if (++kw == KW) {
+      kw = 0;
+      if (++kh == KH) { kh = 0; ++c; }
+    }
+  }
+};
+
+// Bit b of w as 0/1, on the FMA pipe: high word of (w * 2^(31-b)) * two, two = 2.
+__device__ __forceinline__ uint32_t bit01(uint32_t w, uint32_t lift, uint32_t two) {
+  return __umulhi(w * lift, two);
+}
+
 // ---------------------------------------------------------------------------
 // conv2d: one thread = one output pixel x one group of 32 output channels.
 // Lanes of every register are the 32 output channels (the paper's tiling of
@@ -108,6 +124,87 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// conv2d with prepared weights and prepared activations.
+//
+// The activation x is one scalar per thread (broadcast across the 32
+// output-channel lanes), so its class and fraction select a row of the
+// per-weight table built by hobf_prepare_weights (row = frac for a normal x,
+// 2^wF + {0,1,2} for x = zero / inf / NaN; the table holds, for every lane,
+// the rounded significand product, eb - bias + carry, the weight sign and the
+// product class).  The remaining multiplier gates (activation exponent add,
+// overflow / underflow, sign) and the whole adder run as generated lop3 code
+// (F::mac_tab).
+//
+// Activations come as records (hobf_prepare_activations): one uint32 per
+// element in a zero-padded [n][c][h+2p][w+2p] layout, holding the x word in
+// bits [0, 20) and its table row in bits [20, 32).  Per tap a thread does one
+// coalesced 4-byte load (consecutive threads = consecutive output columns),
+// no bounds check (padding records are +0), and FMA-pipe work only: the row
+// is IMAD.HI(rec, 2^12), the exponent / sign bits are broadcast with
+// IMAD (rec * 2^(31-j)) + IMAD.HI (by 1); the ALU pipe is left to the gates.
+// grid = (ceil(npix / 128), ceil(cout / 32)); one CTA = one group of 32
+// output channels, so every warp of the CTA reads the same table block.
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(128) conv_tab_kernel(ConvArgs a) {
+  const int G = (a.cout + 31) >> 5;
+  const int g = blockIdx.y;
+  const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix >= (int64_t)a.n * a.ho * a.wo) return;
+  const int ox = (int)(pix % a.wo);
+  const int oy = (int)((pix / a.wo) % a.ho);
+  const int ni = (int)(pix / ((int64_t)a.wo * a.ho));
+  const int Hp = a.h + 2 * a.pad, Wp = a.w + 2 * a.pad;
+  constexpr int WF = F::WF, WE = F::WE;
+
+  uint32_t acc[F::NOUT];
+#pragma unroll
+  for (int j = 0; j < F::NOUT; j++) acc[j] = 0u;  // +0 (L9)
+
+  // record of (ni, c, oy*stride + kh, ox*stride + kw) = rbase[c*Hp*Wp + kh*Wp + kw]
+  const uint32_t* __restrict__ rbase =
+      a.x + ((int64_t)ni * a.cin * Hp + (int64_t)oy * a.stride) * Wp + (int64_t)ox * a.stride;
+  const int64_t tstride = (int64_t)G * F::TAB_ROWS * F::NPT;  // next (kh, kw, c) table block
+  const uint32_t* __restrict__ tbase = a.wt + (int64_t)g * F::TAB_ROWS * F::NPT;
+  const int64_t cstride = (int64_t)Hp * Wp;
+#pragma unroll 1
+  for (int c = 0; c < a.cin; c++) {
+#pragma unroll 1
+    for (int kh = 0; kh < a.kh; kh++) {
+#pragma unroll 1
+      for (int kw = 0; kw < a.kw; kw++) {
+        const uint32_t rec = __ldg(rbase + c * cstride + kh * Wp + kw);
+        uint32_t EA[WE], SX[1];
+#pragma unroll
+        for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
+        SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
+        const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
+        const uint32_t* pt = tbase + ((int64_t)(kh * a.kw + kw) * a.cin + c) * tstride + (int64_t)row * F::NPT;
+        uint32_t T[F::NPT];
+        const uint4* pt4 = reinterpret_cast<const uint4*>(pt);
+#pragma unroll
+        for (int q = 0; q < F::NPT / 4; q++) {
+          const uint4 v = __ldg(pt4 + q);
+          T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
+        }
+        F::mac_tab(acc, T, EA, SX);
+      }
+    }
+  }
+  if (a.relu) F::relu(acc, acc);
+  uint4* py = reinterpret_cast<uint4*>(a.y + (pix * G + g) * F::NPO);
+#pragma unroll
+  for (int q = 0; q < F::NPO / 4; q++) {
+    uint4 v;
+    v.x = (4 * q + 0 < F::NOUT) ? acc[(4 * q + 0) % F::NOUT] : 0u;
+    v.y = (4 * q + 1 < F::NOUT) ? acc[(4 * q + 1) % F::NOUT] : 0u;
+    v.z = (4 * q + 2 < F::NOUT) ? acc[(4 * q + 2) % F::NOUT] : 0u;
+    v.w = (4 * q + 3 < F::NOUT) ? acc[(4 * q + 3) % F::NOUT] : 0u;
+    py[q] = v;
+  }
+}
+
 // mac_planes: acc[i] = add(acc[i], mul(a[i], b[i])) lane-wise on plane groups.
 template <class F>
 __global__ void __launch_bounds__(256) mac_planes_kernel(uint32_t* __restrict__ acc_p, const uint32_t* __restrict__ a_p,
@@ -134,6 +231,16 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
 }
 
 template <class F>
+cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
+  const int64_t npix = (int64_t)a.n * a.ho * a.wo;
+  if (npix == 0) return cudaSuccess;
+  const int threads = 128;
+  dim3 grid((unsigned)((npix + threads - 1) / threads), (unsigned)((a.cout + 31) / 32));
+  conv_tab_kernel<F><<<grid, threads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <class F>
 cudaError_t launch_mac(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
@@ -151,4 +258,7 @@ cudaError_t launch_mac(uint32_t* acc, const uint32_t* x, const uint32_t* w, int6
   cudaError_t hobf_launch_mac_##TAG(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n,        \
                                     cudaStream_t s) {                                                       \
     return hobf::launch_mac<hobf_gen::F_##TAG>(acc, x, w, n, s);                                            \
+  }                                                                                                         \
+  cudaError_t hobf_launch_convtab_##TAG(const hobf::ConvArgs& a, cudaStream_t s) {                         \
+    return hobf::launch_conv_tab<hobf_gen::F_##TAG>(a, s);                                                  \
   }

@@ -113,15 +113,16 @@ def multiply(g: AIG, a, b):
     return ripple_add(g, r0, r1, FALSE, width=W)
 
 
-def shift_right_sticky(g: AIG, v, d, order="small_first"):
+def shift_right_sticky(g: AIG, v, d, order="small_first", kill=FALSE):
     """Logical right shift of v (LSB first) by the unsigned amount d (bits LSB
-    first); returns (shifted, sticky) where sticky = OR of all bits shifted out."""
+    first); returns (shifted, sticky) where sticky = OR of all bits shifted out.
+    If ``kill`` is true the result and the sticky are forced to zero."""
     W = len(v)
     K = 0
     while (1 << K) <= W:
         K += 1
     K = min(K, len(d))
-    big = g.OR_many(d[K:])
+    big = g.OR(g.OR_many(d[K:]), kill)
     cur = list(v)
     sticky = FALSE
     stages = list(range(K)) if order == "small_first" else list(reversed(range(K)))
@@ -131,7 +132,7 @@ def shift_right_sticky(g: AIG, v, d, order="small_first"):
         sticky = g.OR(sticky, g.AND(d[j], out_bits))
         cur = [g.MUX(d[j], cur[i + sh] if i + sh < W else FALSE, cur[i]) for i in range(W)]
     if big != FALSE:
-        anyv = g.OR_many(v)
+        anyv = g.AND(g.OR_many(v), g.NOT(kill))
         sticky = g.MUX(big, anyv, sticky)
         cur = [g.AND(g.NOT(big), x) for x in cur]
     return cur, sticky
@@ -234,9 +235,35 @@ def fp_mul(g: AIG, A: FP, B: FP, wfo: int, rnd: int):
 
 # --------------------------------------------------------------------------- FP adder
 
+class Operand:
+    """Decoded adder operand.  ``canonical`` operands have exp = frac = 0
+    whenever they are not normal; a non-canonical operand carries exact class
+    flags but arbitrary exp/frac bits when zero, inf or NaN."""
+
+    def __init__(self, we, wf, frac, exp, sign, norm, zero, inf, nan, special, canonical=True):
+        self.we, self.wf = we, wf
+        self.frac, self.exp, self.sign = list(frac), list(exp), sign
+        self.norm, self.zero, self.inf, self.nan, self.special = norm, zero, inf, nan, special
+        self.canonical = canonical
+
+    @staticmethod
+    def from_word(g: AIG, A: FP):
+        nan = g.AND(A.exc1, A.exc0)
+        inf = g.AND(A.exc1, g.NOT(A.exc0))
+        norm = g.AND(g.NOT(A.exc1), A.exc0)
+        zero = g.AND(g.NOT(A.exc1), g.NOT(A.exc0))
+        return Operand(A.we, A.wf, A.frac, A.exp, A.sign, norm, zero, inf, nan, A.exc1, True)
+
+
 def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
+    """HOBFLOPS adder on two canonical words (see fp_add_ops)."""
+    return fp_add_ops(g, Operand.from_word(g, A), Operand.from_word(g, B), rnd, shift_order)
+
+
+def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_first"):
     """HOBFLOPS adder F(wE,w) + F(wE,w) -> F(wE,w) (single-path, P:190-198;
-    SURVEY 8(c) add; ledger L5-L7).
+    SURVEY 8(c) add; ledger L5-L7).  A must be canonical; B may be
+    non-canonical (its exp/frac are ignored when it is zero or special).
 
     Magnitude compare of (exp, frac) and swap so that |X| >= |Y|; alignment
     right shift of 1.fY by eX - eY with guard, round and sticky; effective
@@ -244,21 +271,20 @@ def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
     exponent eX + 1 - lzc + round-carry; overflow -> inf, underflow -> zero,
     exact cancellation -> +0, (-0) + (-0) -> -0.
 
-    Zero operands are canonical (exp = frac = 0) and get hidden bit 0, so they
-    sort below every normal (or tie with exp=0,frac=0 normals, which share
-    their exponent) and flow through the datapath: 0 + y = y exactly."""
+    Canonical zero operands have exp = frac = 0 and hidden bit 0, so they
+    sort below every normal (the hidden bit is the least significant compare
+    key, which breaks the tie with the exp=0, frac=0 normal) and flow through
+    the datapath: 0 + y = y exactly.  A non-canonical zero B never swaps to X
+    and is killed in the aligner."""
     we, w = A.we, A.wf
     p = w + 1
-    nA, nB = g.AND(A.exc1, A.exc0), g.AND(B.exc1, B.exc0)
-    iA, iB = g.AND(A.exc1, g.NOT(A.exc0)), g.AND(B.exc1, g.NOT(B.exc0))
-    hA, hB = g.AND(g.NOT(A.exc1), A.exc0), g.AND(g.NOT(B.exc1), B.exc0)
-    special = g.OR(A.exc1, B.exc1)
+    hA, hB = A.norm, B.norm
+    special = g.OR(A.special, B.special)
 
-    # |A| < |B| by (exp, frac, hidden): the hidden bit as least significant key
-    # breaks the tie between a zero and the exp=0,frac=0 normal in favour of the normal
     keyA = [hA] + list(A.frac) + list(A.exp)
     keyB = [hB] + list(B.frac) + list(B.exp)
-    swap = less_than(g, keyA, keyB)
+    lt = less_than(g, keyA, keyB)
+    swap = lt if B.canonical else g.AND(lt, g.NOT(B.zero))
     eX = [g.MUX(swap, b, a) for a, b in zip(A.exp, B.exp)]
     eY = [g.MUX(swap, a, b) for a, b in zip(A.exp, B.exp)]
     fX = [g.MUX(swap, b, a) for a, b in zip(A.frac, B.frac)]
@@ -267,13 +293,14 @@ def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
     hY = g.MUX(swap, hA, hB)
     sX = g.MUX(swap, B.sign, A.sign)
     sub = g.XOR(A.sign, B.sign)
+    kill = FALSE if B.canonical else g.AND(g.NOT(swap), B.zero)
 
     # d = eX - eY >= 0
     d = ripple_add(g, eX, [g.NOT(x) for x in eY], TRUE, width=we)
     # alignment: W = p + 2 positions (significand + G + R), then sticky
     W = p + 2
     mY = [FALSE, FALSE] + list(fY) + [hY]
-    yv, ys = shift_right_sticky(g, mY, d, order=shift_order)
+    yv, ys = shift_right_sticky(g, mY, d, order=shift_order, kill=kill)
     mX = [FALSE, FALSE] + list(fX) + [hX]
     # adder over W+1 bits: position 0 = sticky, 1..W = shifted significand
     xo = [FALSE] + mX
@@ -301,13 +328,13 @@ def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
     unf = E[EW - 1]
     ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])
 
-    nan = g.OR_many([nA, nB, g.AND(g.AND(iA, iB), sub)])
+    nan = g.OR_many([A.nan, B.nan, g.AND(g.AND(A.inf, B.inf), sub)])
     fin_nz = g.AND(g.NOT(special), g.NOT(zsum))
     normal = g.AND(fin_nz, g.AND(g.NOT(ovf), g.NOT(unf)))
     exc1 = g.OR(special, g.AND(fin_nz, ovf))
     exc0 = g.OR(nan, normal)
     zero_sign = g.AND(g.AND(A.sign, B.sign), g.NOT(hA))
-    inf_sign = g.MUX(iA, A.sign, B.sign)
+    inf_sign = g.MUX(A.inf, A.sign, B.sign)
     sign_fin = g.MUX(zsum, zero_sign, sX)
     sign = g.AND(g.NOT(nan), g.MUX(special, inf_sign, sign_fin))
     exp_out = [g.AND(normal, e) for e in E[:we]]
@@ -370,3 +397,57 @@ def build_relu(we, w) -> Circuit:
     a = g.inputs("a", 3 + we + w)
     out = fp_relu(g, FP(a, we, w))
     return Circuit(f"relu_e{we}m{w}", g, [("a", 3 + we + w)], out)
+
+
+# --------------------------------------------------------------------------- weight-table MAC
+
+def tab_entry_width(we: int, wf: int) -> int:
+    """Planes of one weight-table entry: frac (wF+1) | Epart (wE+2) | S | K0 | K1."""
+    return (wf + 1) + (we + 2) + 3
+
+
+def product_from_table(g: AIG, t, ea, sx, we: int, wf: int) -> Operand:
+    """The multiplier output as an adder operand, from a weight-table entry
+    (rows: x normal with fraction fa -> row fa; x zero -> row 2^wF; x inf ->
+    row 2^wF + 1; x NaN -> row 2^wF + 2).
+
+    The conv broadcasts the activation x across the 32 output-channel lanes
+    (P:257), so x is one scalar per thread: its fraction selects a row of a
+    per-weight table built once from the weight (kernels pre-transformed),
+    holding for every lane the rounded product fraction (round to wF+1 bits at
+    the product's own binade, RNE/RTZ), Epart = eb - bias + (normalise +
+    round carry) as a wE+2-bit two's complement number, the weight sign and the
+    product class (K1 K0: 00 zero, 01 normal, 10 inf, 11 NaN; rows for x =
+    zero / inf / NaN encode the exception algebra of S:68).  The gates left
+    add the activation exponent, classify overflow / underflow (ledger L5, L6)
+    and combine the signs."""
+    wfo = wf + 1
+    EW = we + 2
+    F = t[0:wfo]
+    Ep = t[wfo:wfo + EW]
+    S, K0, K1 = t[wfo + EW], t[wfo + EW + 1], t[wfo + EW + 2]
+    E = ripple_add(g, Ep, list(ea), FALSE, width=EW)
+    unf = E[EW - 1]
+    ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])
+    nK1 = g.NOT(K1)
+    norm = g.AND(g.AND(nK1, K0), g.AND(g.NOT(ovf), g.NOT(unf)))
+    zero = g.AND(nK1, g.OR(g.NOT(K0), unf))
+    inf = g.OR(g.AND(K1, g.NOT(K0)), g.AND(g.AND(nK1, K0), ovf))
+    nan = g.AND(K1, K0)
+    special = g.OR(K1, g.AND(K0, ovf))
+    sign = g.XOR(S, sx)
+    return Operand(we, wfo, F, E[:we], sign, norm, zero, inf, nan, special, canonical=False)
+
+
+def build_mac_tab(we, wf, rnd, **kw) -> Circuit:
+    """acc' = add(acc, mul(x, w)) with the multiplier read from the weight table."""
+    wfo = wf + 1
+    g = AIG()
+    acc = g.inputs("acc", 3 + we + wfo)
+    t = g.inputs("t", tab_entry_width(we, wf))
+    ea = g.inputs("ea", we)
+    sx = g.inputs("sx", 1)[0]
+    B = product_from_table(g, t, ea, sx, we, wf)
+    out = fp_add_ops(g, Operand.from_word(g, FP(acc, we, wfo)), B, rnd, **kw)
+    return Circuit(f"mactab_e{we}m{wf}_{'rne' if rnd == RNE else 'rtz'}", g,
+                   [("acc", 3 + we + wfo), ("t", tab_entry_width(we, wf)), ("ea", we), ("sx", 1)], out)

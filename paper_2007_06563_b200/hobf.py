@@ -83,8 +83,18 @@ _lib.hobf_conv2d.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i3
 _lib.hobf_mac_planes.restype = _i32
 _lib.hobf_mac_planes.argtypes = [hobf_fmt, _p, _p, _p, _i64, _p]
 _lib.hobf_gate_count.restype = _i32
-_lib.hobf_gate_count.argtypes = [hobf_fmt, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
-                                 ctypes.POINTER(_i32)]
+_lib.hobf_gate_count.argtypes = [hobf_fmt] + [ctypes.POINTER(_i32)] * 5
+_lib.hobf_wtab_words.restype = _i64
+_lib.hobf_wtab_words.argtypes = [hobf_fmt, _i32, _i32, _i32, _i32]
+_lib.hobf_prepare_weights.restype = _i32
+_lib.hobf_prepare_weights.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _p]
+_lib.hobf_conv2d_prepared.restype = _i32
+_lib.hobf_conv2d_prepared.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _i32,
+                                      _p, _p]
+_lib.hobf_xrec_words.restype = _i64
+_lib.hobf_xrec_words.argtypes = [_i32, _i32, _i32, _i32, _i32]
+_lib.hobf_prepare_activations.restype = _i32
+_lib.hobf_prepare_activations.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _i32, _p, _p]
 _lib.hobf_lop3_peak.restype = _i32
 _lib.hobf_lop3_peak.argtypes = [_i32, _i32, _i32, _p, _p, ctypes.POINTER(_i64)]
 _lib.hobf_last_launch_count.restype = _i32
@@ -94,7 +104,9 @@ _lib.hobf_version.restype = ctypes.c_char_p
 
 SYMBOLS = ["hobf_nbits", "hobf_out_wf", "hobf_nplanes", "hobf_planes_words", "hobf_pack", "hobf_quantize_pack",
            "hobf_unpack", "hobf_unpack_f32", "hobf_conv2d", "hobf_mac_planes", "hobf_gate_count",
-           "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version"]
+           "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version",
+           "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_xrec_words",
+           "hobf_prepare_activations"]
 
 
 def _check(fn, st):
@@ -203,9 +215,51 @@ def mac_planes(f: Fmt, acc: torch.Tensor, a: torch.Tensor, b: torch.Tensor, stre
 
 
 def gate_count(f: Fmt) -> dict:
-    v = [_i32() for _ in range(4)]
+    v = [_i32() for _ in range(5)]
     _check("hobf_gate_count", _lib.hobf_gate_count(f.c(), *[ctypes.byref(x) for x in v]))
-    return {"mac": v[0].value, "mul": v[1].value, "add": v[2].value, "relu": v[3].value}
+    return {"mac": v[0].value, "mul": v[1].value, "add": v[2].value, "relu": v[3].value, "mac_tab": v[4].value}
+
+
+def wtab_words(f: Fmt, kh: int, kw: int, cin: int, cout: int) -> int:
+    """Size of the prepared-weight table in words, or -1 if the format has no table kernel."""
+    return _lib.hobf_wtab_words(f.c(), kh, kw, cin, cout)
+
+
+def prepare_weights(f: Fmt, w_planes: torch.Tensor, kh: int, kw: int, cin: int, cout: int, out=None,
+                    stream=None) -> torch.Tensor:
+    n = wtab_words(f, kh, kw, cin, cout)
+    if n < 0:
+        raise HobfError("hobf_wtab_words", 3)
+    if out is None:
+        out = torch.empty(n, dtype=torch.int32, device=w_planes.device)
+    _check("hobf_prepare_weights", _lib.hobf_prepare_weights(f.c(), _ptr(w_planes), kh, kw, cin, cout, _ptr(out),
+                                                             _stream(stream)))
+    return out
+
+
+def xrec_words(n: int, h: int, w: int, cin: int, pad: int) -> int:
+    return _lib.hobf_xrec_words(n, h, w, cin, pad)
+
+
+def prepare_activations(f: Fmt, x_planes: torch.Tensor, n: int, h: int, w: int, cin: int, pad: int, out=None,
+                        stream=None) -> torch.Tensor:
+    """Activation planes -> zero-padded [n][cin][h+2pad][w+2pad] records for conv2d_prepared."""
+    if out is None:
+        out = torch.empty(max(xrec_words(n, h, w, cin, pad), 1), dtype=torch.int32, device=x_planes.device)
+    _check("hobf_prepare_activations", _lib.hobf_prepare_activations(f.c(), _ptr(x_planes), n, h, w, cin, pad,
+                                                                     _ptr(out), _stream(stream)))
+    return out
+
+
+def conv2d_prepared(f: Fmt, xrec: torch.Tensor, n: int, h: int, w: int, cin: int, wtab: torch.Tensor,
+                    kh: int, kw: int, cout: int, stride: int = 1, pad: int = 1, relu: int = 0, out=None,
+                    stream=None) -> torch.Tensor:
+    """Conv on prepared activations (same pad) and prepared weights -> output planes."""
+    ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
+    out = _new_planes(max(n * ho * wo, 0), cout, f.nout, xrec.device, out)
+    _check("hobf_conv2d_prepared", _lib.hobf_conv2d_prepared(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw,
+                                                             cout, stride, pad, int(relu), _ptr(out), _stream(stream)))
+    return out
 
 
 def lop3_peak(blocks: int, threads: int, iters: int, sink: torch.Tensor, stream=None) -> int:
@@ -222,13 +276,21 @@ class Conv2d:
     NHWC input, runs the bitsliced conv and unpacks the NHWC float32 output
     (exact in float32), all in CUDA kernels."""
 
-    def __init__(self, weight_f32: torch.Tensor, f: Fmt, stride: int = 1, pad: int = 1, relu: bool = False):
+    def __init__(self, weight_f32: torch.Tensor, f: Fmt, stride: int = 1, pad: int = 1, relu: bool = False,
+                 use_tables: bool = True):
         kh, kw, cin, cout = weight_f32.shape
         self.f, self.kh, self.kw, self.cin, self.cout = f, kh, kw, cin, cout
         self.stride, self.pad, self.relu = stride, pad, relu
         self.w_planes = quantize_pack(f.we, f.wf, weight_f32.reshape(kh * kw * cin, cout).contiguous(), f.round)
+        self.wtab = None
+        if use_tables and wtab_words(f, kh, kw, cin, cout) > 0:
+            self.wtab = prepare_weights(f, self.w_planes, kh, kw, cin, cout)
 
     def forward_planes(self, x_planes, n, h, w, out=None, stream=None):
+        if self.wtab is not None:
+            xrec = prepare_activations(self.f, x_planes, n, h, w, self.cin, self.pad, stream=stream)
+            return conv2d_prepared(self.f, xrec, n, h, w, self.cin, self.wtab, self.kh, self.kw, self.cout,
+                                   self.stride, self.pad, int(self.relu), out=out, stream=stream)
         return conv2d(self.f, x_planes, n, h, w, self.cin, self.w_planes, self.kh, self.kw, self.cout,
                       self.stride, self.pad, int(self.relu), out=out, stream=stream)
 

@@ -1,0 +1,67 @@
+"""Weight-table entries for the prepared-weights MAC circuit (tests only).
+
+Vectorised numpy statement of what one table entry holds (see
+include/hobf.h hobf_wtab_words and gen/fpgen.product_from_table), used to
+drive the generated ``mac_tab`` circuit on CPU so that circuit + table
+semantics can be checked exhaustively against the oracle.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def row_of(x, we, wf):
+    """Table row selected by activation word x: fraction if normal; 2^wf + 0/1/2 for zero/inf/NaN."""
+    x = np.asarray(x, dtype=np.int64)
+    exc = (x >> (wf + we + 1)) & 3
+    fa = x & ((1 << wf) - 1)
+    special = np.select([exc == 0, exc == 2, exc == 3], [0, 1, 2], 0)
+    return np.where(exc == 1, fa, (1 << wf) + special)
+
+
+def entries(w, r, we, wf, rnd):
+    w = np.asarray(w, dtype=np.int64)
+    r = np.asarray(r, dtype=np.int64)
+    wfo, EW = wf + 1, we + 2
+    exc = (w >> (wf + we + 1)) & 3
+    sw = (w >> (wf + we)) & 1
+    eb = (w >> wf) & ((1 << we) - 1)
+    fb = w & ((1 << wf) - 1)
+    sbit = wfo + EW
+    NAN = (1 << (sbit + 1)) | (1 << (sbit + 2))
+    INF = (1 << (sbit + 2)) | (sw << sbit)
+    ZERO = sw << sbit
+    nrows = 1 << wf
+    # both normal: exact product (1.fa)(1.fb), round to wfo fraction bits at its binade
+    ma = (1 << wf) | np.minimum(r, nrows - 1)
+    mb = (1 << wf) | fb
+    P = ma * mb
+    top = (P >> (2 * wf + 1)) & 1
+    N = np.where(top == 1, P, P << 1)
+    kept = N >> wf
+    rem = N & ((1 << wf) - 1)
+    half = 1 << (wf - 1)
+    if rnd == 0:
+        kept = kept + ((rem > half) | ((rem == half) & ((kept & 1) == 1)))
+    inc = top.copy()
+    carry = kept == (2 << wfo)
+    kept = np.where(carry, kept >> 1, kept)
+    inc = inc + carry
+    frac = kept - (1 << wfo)
+    bias = (1 << (we - 1)) - 1
+    ep = (eb - bias + inc) & ((1 << EW) - 1)
+    normal_e = frac | (ep << wfo) | (sw << sbit) | (1 << (sbit + 1))
+    out = np.select([exc == 0, exc == 2, exc == 3], [ZERO, INF, NAN], normal_e)
+    out = np.where(r == nrows, np.where((exc & 2) != 0, NAN, ZERO), out)
+    out = np.where(r == nrows + 1, np.where((exc == 0) | (exc == 3), NAN, INF), out)
+    out = np.where(r == nrows + 2, NAN, out)
+    return out.astype(np.uint32)
+
+
+def circuit_inputs(acc, x, w, we, wf, rnd):
+    """Arrays for build_mac_tab's inputs (acc, t, ea, sx) for lane-wise (acc, x, w)."""
+    x = np.asarray(x, dtype=np.int64)
+    t = entries(w, row_of(x, we, wf), we, wf, rnd)
+    ea = ((x >> wf) & ((1 << we) - 1)).astype(np.uint32)
+    sx = ((x >> (wf + we)) & 1).astype(np.uint32)
+    return [np.asarray(acc, np.uint32), t, ea, sx]

@@ -184,3 +184,44 @@ def test_emitted_headers_up_to_date(tmp_path):
 def test_emitted_mac_lop3_count_matches_mapping():
     r = emit.gen_format(5, 3, 0)
     assert r["src"].count("hobf_lop3<") == r["g_mac"] + r["g_relu"]
+
+
+# ----------------------------------------------------------------------------- prepared-weights (table) MAC
+
+import tabref  # noqa: E402
+
+
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 3), (5, 2), (6, 2)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mac_tab_exhaustive_pairs(we, wf, rnd):
+    """Table MAC circuit fed with table entries (tests/tabref.py) equals the
+    oracle MAC for every (x, w) pair of canonical operands against a spread of
+    accumulators (every 23rd canonical accumulator, plus all specials)."""
+    c = fpgen.build_mac_tab(we, wf, rnd)
+    m = lutmap.map_aig(c.g, c.outputs)
+    xi = canon_words(we, wf)
+    X, W = np.meshgrid(xi, xi, indexing="ij")
+    X, W = X.ravel(), W.ravel()
+    acc_all = canon_words(we, wf + 1)
+    accs = np.concatenate([acc_all[:5], acc_all[5::23]])
+    for s in range(0, accs.size, 8):
+        a = accs[s:s + 8]
+        A = np.repeat(a, X.size)
+        XX, WW = np.tile(X, a.size), np.tile(W, a.size)
+        _check(c, m, tabref.circuit_inputs(A, XX, WW, we, wf, rnd), oracle.mac(A, XX, WW, we, wf, wf + 1, rnd))
+
+
+@pytest.mark.parametrize("we,wf", [(5, 7), (4, 6), (6, 5)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mac_tab_random(we, wf, rnd):
+    rng = np.random.default_rng(we * 13 + wf * 3 + rnd)
+    N = 200_000
+    c = fpgen.build_mac_tab(we, wf, rnd)
+    m = lutmap.map_aig(c.g, c.outputs)
+    acc = _rand_words(rng, N, we, wf + 1)
+    x = _rand_words(rng, N, we, wf)
+    w = _rand_words(rng, N, we, wf)
+    half = N // 2
+    p = oracle.mul(x[:half], w[:half], we, wf, wf + 1, rnd)
+    acc[:half] = np.where(rng.random(half) < 0.5, p ^ np.uint32(1 << (wf + 1 + we)), acc[:half])
+    _check(c, m, tabref.circuit_inputs(acc, x, w, we, wf, rnd), oracle.mac(acc, x, w, we, wf, wf + 1, rnd))

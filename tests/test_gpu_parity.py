@@ -185,18 +185,25 @@ def test_gate_counts_reported():
         for rnd, name in ((0, "rne"), (1, "rtz")):
             g = H.gate_count(H.Fmt(we, wf, rnd))
             assert g["mac"] == counts[f"e{we}m{wf}_{name}"]["g_mac"]
+            assert g["mac_tab"] == counts[f"e{we}m{wf}_{name}"]["g_tab"]
 
 
 # ----------------------------------------------------------------------------- conv
 
-def gpu_conv(x_f32, w_f32, f, stride=1, pad=1, relu=0):
-    """float32 NHWC x and KhKwCinCout w -> quantise+pack on GPU -> conv -> unpack words."""
+def gpu_conv(x_f32, w_f32, f, stride=1, pad=1, relu=0, prepared=False):
+    """float32 NHWC x and KhKwCinCout w -> quantise+pack on GPU -> conv -> unpack words.
+    prepared=True runs hobf_prepare_weights + hobf_conv2d_prepared (weight tables)."""
     H = hobf()
     n, h, w, cin = x_f32.shape
     kh, kw, _, cout = w_f32.shape
     xp = H.quantize_pack(f.we, f.wf, torch.from_numpy(x_f32.reshape(-1, cin)).cuda(), f.round)
     wp = H.quantize_pack(f.we, f.wf, torch.from_numpy(w_f32.reshape(-1, cout)).cuda(), f.round)
-    yp = H.conv2d(f, xp, n, h, w, cin, wp, kh, kw, cout, stride, pad, relu)
+    if prepared:
+        wt = H.prepare_weights(f, wp, kh, kw, cin, cout)
+        xr = H.prepare_activations(f, xp, n, h, w, cin, pad)
+        yp = H.conv2d_prepared(f, xr, n, h, w, cin, wt, kh, kw, cout, stride, pad, relu)
+    else:
+        yp = H.conv2d(f, xp, n, h, w, cin, wp, kh, kw, cout, stride, pad, relu)
     ho, wo = H.conv_out_hw(h, w, kh, kw, stride, pad)
     y = to_np_words(H.unpack(f.we, f.wfo, yp, n * ho * wo, cout)).reshape(n, ho, wo, cout)
     return y
@@ -221,6 +228,22 @@ def test_conv_C1_full():
             assert np.array_equal(got, exp), (rnd, relu, np.argwhere(got != exp)[:5])
 
 
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 3), (6, 2), (4, 7)])
+def test_conv_prepared_full_vs_oracle(we, wf):
+    """The weight-table path in full on a C1-shaped layer with every special class present."""
+    H = hobf()
+    x, w = inputs.small_case(77, 2, 8, 8, 48, 64)
+    x[0, 0, :4, 0] = [np.inf, -np.inf, np.nan, -0.0]
+    w[0, 0, 1, :3] = [np.inf, np.nan, 0.0]
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd)
+        for relu in (0, 1):
+            got = gpu_conv(x, w, f, relu=relu, prepared=True)
+            exp = oracle_conv(x, w, f, relu=relu)
+            assert np.array_equal(got, exp), (rnd, relu, np.argwhere(got != exp)[:5])
+            assert np.array_equal(got, gpu_conv(x, w, f, relu=relu, prepared=False))
+
+
 @pytest.mark.parametrize("shape", [
     # n, h, w, cin, cout, kh, kw, stride, pad
     (2, 9, 7, 40, 50, 3, 3, 1, 1),     # ragged cin and cout, several tiles
@@ -230,20 +253,22 @@ def test_conv_C1_full():
     (1, 7, 7, 5, 32, 5, 5, 1, 2),      # 5x5 kernel
     (1, 1, 1, 16, 32, 3, 3, 1, 1),     # 1x1 image: every tap but the centre is padding
 ])
-@pytest.mark.parametrize("we,wf", [(5, 3), (4, 3), (5, 10), (6, 7)])
-def test_conv_small_shapes(shape, we, wf):
+@pytest.mark.parametrize("we,wf,prepared", [(5, 3, 0), (4, 3, 0), (5, 10, 0), (6, 7, 0),
+                                             (5, 3, 1), (4, 3, 1), (6, 7, 1), (4, 2, 1), (5, 5, 1)])
+def test_conv_small_shapes(shape, we, wf, prepared):
     H = hobf()
     n, h, w, cin, cout, kh, kw, stride, pad = shape
     x, wt = inputs.small_case(sum(shape) + we + wf, n, h, w, cin, cout, "normal", 0.5, kh, kw)
     for rnd in (0, 1):
         f = H.Fmt(we, wf, rnd)
         relu = rnd  # alternate
-        got = gpu_conv(x, wt, f, stride, pad, relu)
+        got = gpu_conv(x, wt, f, stride, pad, relu, prepared=bool(prepared))
         exp = oracle_conv(x, wt, f, stride, pad, relu)
         assert np.array_equal(got, exp), np.argwhere(got != exp)[:5]
 
 
-def test_conv_specials_propagate():
+@pytest.mark.parametrize("prepared", [False, True])
+def test_conv_specials_propagate(prepared):
     """inf / NaN / overflow inputs: 0*inf = NaN through padding taps, inf + -inf = NaN."""
     H = hobf()
     f = H.Fmt(5, 3, 0)
@@ -256,14 +281,16 @@ def test_conv_specials_propagate():
     w[1, 1, 0, :] = np.inf
     w[0, 2, 5, 7] = -np.inf
     w[2, 2, 6, :] = 3e4
+    x[0, 1, 3, 4] = 1e-4      # tiny: products underflow to zero
+    w[1, 0, 4, 3] = -2e-5
     for relu in (0, 1):
-        got = gpu_conv(x, w, f, relu=relu)
+        got = gpu_conv(x, w, f, relu=relu, prepared=prepared)
         exp = oracle_conv(x, w, f, relu=relu)
         assert np.array_equal(got, exp)
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
-def test_conv_configs_sampled(name):
+@pytest.mark.parametrize("name,prepared", [("C2", 0), ("C3", 0), ("C4", 0), ("C3", 1), ("C4", 1)])
+def test_conv_configs_sampled(name, prepared):
     """Full-size configs in the bench launch configuration, checked on sampled
     outputs the oracle computes one by one."""
     H = hobf()
@@ -271,7 +298,7 @@ def test_conv_configs_sampled(name):
     x, w = inputs.draw(cfg)
     we, wf = cfg.formats[0]
     f = H.Fmt(we, wf, 0)
-    got = gpu_conv(x, w, f)
+    got = gpu_conv(x, w, f, prepared=bool(prepared))
     xq = oracle.encode_f32(x, we, wf, 0)
     wq = oracle.encode_f32(w, we, wf, 0)
     rng = np.random.default_rng(5)
@@ -288,7 +315,7 @@ def test_conv_C5_sweep_sampled():
     rng = np.random.default_rng(6)
     for (we, wf) in cfg.formats:
         f = H.Fmt(we, wf, 0)
-        got = gpu_conv(x, w, f)
+        got = gpu_conv(x, w, f, prepared=H.wtab_words(f, 3, 3, cfg.cin, cfg.cout) > 0)
         xq = oracle.encode_f32(x, we, wf, 0)
         wq = oracle.encode_f32(w, we, wf, 0)
         idx = rng.integers(0, got.size, 150)
