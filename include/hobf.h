@@ -122,7 +122,7 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
  * Results are identical to hobf_conv2d.
  *
  * hobf_wtab_words: size in uint32 words of the table buffer for these weights,
- * or -1 if the format has no table kernel (wf > 7, extended class).
+ * or -1 if the format has no table kernel (wf > 10, extended class).
  * Layout: [kh][kw][cin][ceil(cout/32)][2^wf + 3 rows][roundup(wf + we + 6, 4) planes]. */
 int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t cout);
 

@@ -160,7 +160,7 @@ static unsigned warp_grid(int64_t items) {
 
 // ----------------------------------------------------------------------------- weight tables
 // Largest wF with a prepared-weights (table) kernel; the table has 2^wF + 3 rows.
-static const int kTabMaxWf = 7;
+static const int kTabMaxWf = 10;
 
 __host__ __device__ static inline int tab_width(int we, int wf) { return (wf + 1) + (we + 2) + 3; }
 __host__ __device__ static inline int tab_rows(int wf) { return (1 << wf) + 3; }
@@ -194,7 +194,7 @@ __device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int rnd) {
   if (exc == 3u) return NAN_E;
   // both normal: exact significand product, normalise, round to wfo bits
   const uint32_t ma = (1u << wf) | (uint32_t)r, mb = (1u << wf) | fb;
-  const uint32_t P = ma * mb;  // < 2^(2wf+2) <= 2^16 for wf <= 7
+  const uint32_t P = ma * mb;  // < 2^(2wf+2) <= 2^22 for wf <= 10
   const uint32_t top = (P >> (2 * wf + 1)) & 1u;
   const uint32_t N = top ? P : (P << 1);       // leading one at bit 2wf+1
   uint32_t kept = N >> wf;                     // wfo+1 bits
@@ -453,7 +453,7 @@ static int conv_tab_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HOBF_CONV_VARIANT");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : 0;
   }
   return v;
 }

@@ -146,8 +146,31 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
 // grid = (ceil(npix / 128), ceil(cout / 32)); one CTA = one group of 32
 // output channels, so every warp of the CTA reads the same table block.
 // ---------------------------------------------------------------------------
+// Per-tap operands of the table MAC: broadcast activation exponent / sign
+// planes (FMA pipe) and the table entry the activation's row selects.
 template <class F>
-__global__ void __launch_bounds__(128) conv_tab_kernel(ConvArgs a) {
+struct TabTap {
+  uint32_t EA[F::WE], SX[1], T[F::NPT];
+  __device__ __forceinline__ void load(uint32_t rec, const uint32_t* __restrict__ tblock, const ConvArgs& a) {
+    constexpr int WF = F::WF, WE = F::WE;
+#pragma unroll
+    for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
+    SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
+    const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
+    const uint4* pt4 = reinterpret_cast<const uint4*>(tblock + (int64_t)row * F::NPT);
+#pragma unroll
+    for (int q = 0; q < F::NPT / 4; q++) {
+      const uint4 v = __ldg(pt4 + q);
+      T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
+    }
+  }
+};
+
+// KW3: kernel width fixed at 3 (inner loop unrolled).  PF: software pipeline --
+// the record of tap t+2 and the table entry of tap t+1 are loaded while the
+// MAC of tap t runs (for the latency-bound small-batch configs).
+template <class F, int NT, int MINB, bool KW3, bool PF>
+__global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   const int G = (a.cout + 31) >> 5;
   const int g = blockIdx.y;
   const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -156,7 +179,7 @@ __global__ void __launch_bounds__(128) conv_tab_kernel(ConvArgs a) {
   const int oy = (int)((pix / a.wo) % a.ho);
   const int ni = (int)(pix / ((int64_t)a.wo * a.ho));
   const int Hp = a.h + 2 * a.pad, Wp = a.w + 2 * a.pad;
-  constexpr int WF = F::WF, WE = F::WE;
+  const int KW = KW3 ? 3 : a.kw;
 
   uint32_t acc[F::NOUT];
 #pragma unroll
@@ -168,28 +191,40 @@ __global__ void __launch_bounds__(128) conv_tab_kernel(ConvArgs a) {
   const int64_t tstride = (int64_t)G * F::TAB_ROWS * F::NPT;  // next (kh, kw, c) table block
   const uint32_t* __restrict__ tbase = a.wt + (int64_t)g * F::TAB_ROWS * F::NPT;
   const int64_t cstride = (int64_t)Hp * Wp;
+  auto rec_at = [&](int c, int kh, int kw) { return __ldg(rbase + c * cstride + kh * Wp + kw); };
+  auto tblock = [&](int c, int kh, int kw) { return tbase + ((int64_t)(kh * KW + kw) * a.cin + c) * tstride; };
+
+  if (!PF) {
 #pragma unroll 1
-  for (int c = 0; c < a.cin; c++) {
+    for (int c = 0; c < a.cin; c++) {
 #pragma unroll 1
-    for (int kh = 0; kh < a.kh; kh++) {
-#pragma unroll 1
-      for (int kw = 0; kw < a.kw; kw++) {
-        const uint32_t rec = __ldg(rbase + c * cstride + kh * Wp + kw);
-        uint32_t EA[WE], SX[1];
+      for (int kh = 0; kh < a.kh; kh++) {
 #pragma unroll
-        for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
-        SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
-        const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
-        const uint32_t* pt = tbase + ((int64_t)(kh * a.kw + kw) * a.cin + c) * tstride + (int64_t)row * F::NPT;
-        uint32_t T[F::NPT];
-        const uint4* pt4 = reinterpret_cast<const uint4*>(pt);
-#pragma unroll
-        for (int q = 0; q < F::NPT / 4; q++) {
-          const uint4 v = __ldg(pt4 + q);
-          T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
+        for (int kw = 0; kw < KW; kw++) {
+          TabTap<F> tp;
+          tp.load(rec_at(c, kh, kw), tblock(c, kh, kw), a);
+          F::mac_tab(acc, tp.T, tp.EA, tp.SX);
         }
-        F::mac_tab(acc, T, EA, SX);
       }
+    }
+  } else {
+    TapIter tr, tt;  // tap of the next record / of the next table entry
+    uint32_t rn = rec_at(0, 0, 0);
+    TabTap<F> nxt;
+    nxt.load(rn, tblock(0, 0, 0), a);
+    tt.next(a.kh, KW);
+    tr = tt;
+    rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+    tr.next(a.kh, KW);
+    const int taps = a.cin * a.kh * KW;
+#pragma unroll 1
+    for (int t = 0; t < taps; t++) {
+      TabTap<F> cur = nxt;
+      if (tt.c < a.cin) nxt.load(rn, tblock(tt.c, tt.kh, tt.kw), a);
+      tt.next(a.kh, KW);
+      rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+      tr.next(a.kh, KW);
+      F::mac_tab(acc, cur.T, cur.EA, cur.SX);
     }
   }
   if (a.relu) F::relu(acc, acc);
@@ -234,9 +269,30 @@ template <class F>
 cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const int64_t npix = (int64_t)a.n * a.ho * a.wo;
   if (npix == 0) return cudaSuccess;
-  const int threads = 128;
-  dim3 grid((unsigned)((npix + threads - 1) / threads), (unsigned)((a.cout + 31) / 32));
-  conv_tab_kernel<F><<<grid, threads, 0, s>>>(a);
+  const unsigned gy = (unsigned)((a.cout + 31) / 32);
+  auto grid = [&](int threads) { return dim3((unsigned)((npix + threads - 1) / threads), gy); };
+  const bool k3 = a.kw == 3;
+  int variant = a.variant;
+  if (variant == 0) {
+    // auto: the software-pipelined kernel when the table rows do not stay L1
+    // resident (wF >= 8) or when there are fewer than ~4 warps per SMSP to hide
+    // load latency; otherwise the KW=3-unrolled kernel at <= 56 registers.
+    const int64_t warps = (npix + 31) / 32 * gy;
+    variant = (F::WF >= 8 || warps < 148 * 4 * 4) ? 4 : 3;
+  }
+  switch (variant) {
+    case 1: conv_tab_kernel<F, 128, 1, false, false><<<grid(128), 128, 0, s>>>(a); break;
+    case 3:
+      if (k3) conv_tab_kernel<F, 128, 9, true, false><<<grid(128), 128, 0, s>>>(a);
+      else conv_tab_kernel<F, 128, 9, false, false><<<grid(128), 128, 0, s>>>(a);
+      break;
+    case 4:  // pipelined (latency-bound configs)
+      if (k3) conv_tab_kernel<F, 128, 1, true, true><<<grid(128), 128, 0, s>>>(a);
+      else conv_tab_kernel<F, 128, 1, false, true><<<grid(128), 128, 0, s>>>(a);
+      break;
+    case 5: conv_tab_kernel<F, 64, 1, false, true><<<grid(64), 64, 0, s>>>(a); break;
+    default: conv_tab_kernel<F, 128, 9, false, false><<<grid(128), 128, 0, s>>>(a); break;
+  }
   return cudaGetLastError();
 }
 
