@@ -139,6 +139,10 @@ hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t
 int64_t hobf_xrec_words(int32_t n, int32_t h, int32_t w, int32_t cin, int32_t pad);
 hobf_status hobf_prepare_activations(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w,
                                      int32_t cin, int32_t pad, uint32_t* d_xrec, hobf_stream stream);
+/* float32 NHWC activations (device) -> records directly, quantised with f.round
+ * exactly as hobf_quantize_pack (first layer: no bitslice round trip). */
+hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                      int32_t pad, uint32_t* d_xrec, hobf_stream stream);
 
 /* hobf_conv2d on prepared activations (built with the same pad) and prepared
  * weights; identical results.  Output planes as for hobf_conv2d. */

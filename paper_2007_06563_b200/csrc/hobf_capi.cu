@@ -132,20 +132,30 @@ __global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict_
   const int64_t items = rows * G;
   const int nb = 3 + we + wf;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
-    const uint32_t mine = lane < np ? __ldg(planes + it * np + lane) : 0u;
-    uint32_t v = 0u;
-    for (int j = 0; j < nb; j++) {
-      const uint32_t pj = __shfl_sync(0xffffffffu, mine, j);
-      v |= ((pj >> lane) & 1u) << j;
-    }
-    const int64_t r = it / G;
-    const int64_t c = (it - r * G) * 32 + lane;
-    if (c < C) {
-      if (TO_F32)
-        reinterpret_cast<float*>(dst)[r * C + c] = decode_f32(v, we, wf);
-      else
-        reinterpret_cast<uint32_t*>(dst)[r * C + c] = v;
+  // UNR groups per warp iteration: their plane loads are all in flight before the
+  // shuffles (the loop body is otherwise one dependent load -> shfl -> store chain).
+  constexpr int UNR = 4;
+  for (int64_t it0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * UNR; it0 < items; it0 += nw * UNR) {
+    uint32_t mine[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) mine[u] = (lane < np && it0 + u < items) ? __ldg(planes + (it0 + u) * np + lane) : 0u;
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const int64_t it = it0 + u;
+      if (it >= items) break;
+      uint32_t v = 0u;
+      for (int j = 0; j < nb; j++) {
+        const uint32_t pj = __shfl_sync(0xffffffffu, mine[u], j);
+        v |= ((pj >> lane) & 1u) << j;
+      }
+      const int64_t r = it / G;
+      const int64_t c = (it - r * G) * 32 + lane;
+      if (c < C) {
+        if (TO_F32)
+          reinterpret_cast<float*>(dst)[r * C + c] = decode_f32(v, we, wf);
+        else
+          reinterpret_cast<uint32_t*>(dst)[r * C + c] = v;
+      }
     }
   }
 }
@@ -253,6 +263,34 @@ __global__ void __launch_bounds__(256) prepare_acts_kernel(const uint32_t* __res
         out[(int64_t)(cg * 32 + b) * Hp * Wp] = v;
       }
     }
+  }
+}
+
+// float32 NHWC activations -> quantised records in the padded [n][c][h+2p][w+2p]
+// layout in one pass (the first layer of a network: no bitslice round trip).
+// CTA tile = 32 padded columns x 32 channels of one (n, padded row): coalesced
+// float reads along c, smem transpose, coalesced record writes along columns.
+__global__ void __launch_bounds__(256) quantize_acts_kernel(const float* __restrict__ x, int n, int h, int w, int cin,
+                                                            int pad, int we, int wf, int rnd,
+                                                            uint32_t* __restrict__ rec) {
+  __shared__ uint32_t tile[32][33];
+  const int Hp = h + 2 * pad, Wp = w + 2 * pad;
+  const int xb = blockIdx.x * 32;          // first padded column of the tile
+  const int cb = blockIdx.y * 32;          // first channel of the tile
+  const int ni = blockIdx.z / Hp, iyp = blockIdx.z % Hp;
+  const int iy = iyp - pad;
+  const uint32_t zero_rec = xrec_of(0u, we, wf);
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {  // column within the tile
+    const int ixp = xb + k, ix = ixp - pad, c = cb + threadIdx.x;
+    uint32_t v = zero_rec;
+    if (iy >= 0 && iy < h && ix >= 0 && ix < w && c < cin)
+      v = xrec_of(encode_f32(__ldg(x + (((int64_t)ni * h + iy) * w + ix) * cin + c), we, wf, rnd), we, wf);
+    tile[k][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {  // channel within the tile
+    const int c = cb + k, ixp = xb + threadIdx.x;
+    if (c < cin && ixp < Wp) rec[(((int64_t)ni * cin + c) * Hp + iyp) * Wp + ixp] = tile[threadIdx.x][k];
   }
 }
 
@@ -506,6 +544,25 @@ hobf_status hobf_prepare_activations(hobf_fmt f, const uint32_t* d_x_planes, int
   if (blocks > 148 * 32) blocks = 148 * 32;
   prepare_acts_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_x_planes, n, h, w, cin, pad, f.we, f.wf,
                                                                             d_xrec);
+  if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                                      int32_t pad, uint32_t* d_xrec, hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || n < 0 || h < 0 || w < 0 || cin < 0 || pad < 0)
+    return HOBF_EINVAL;
+  if (h == 0 || w == 0 || cin == 0) return HOBF_ESHAPE;
+  if (!tab_format(f)) return HOBF_EUNSUPPORTED;
+  if (n == 0) return HOBF_OK;
+  if (!d_x || !d_xrec) return HOBF_EINVAL;
+  const int Hp = h + 2 * pad, Wp = w + 2 * pad;
+  if ((int64_t)n * Hp > 2147483647LL) return HOBF_EINVAL;
+  dim3 grid((unsigned)((Wp + 31) / 32), (unsigned)((cin + 31) / 32), (unsigned)(n * Hp));
+  quantize_acts_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(d_x, n, h, w, cin, pad, f.we, f.wf, f.round,
+                                                                      d_xrec);
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;

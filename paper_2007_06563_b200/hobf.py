@@ -95,6 +95,8 @@ _lib.hobf_xrec_words.restype = _i64
 _lib.hobf_xrec_words.argtypes = [_i32, _i32, _i32, _i32, _i32]
 _lib.hobf_prepare_activations.restype = _i32
 _lib.hobf_prepare_activations.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _i32, _p, _p]
+_lib.hobf_quantize_activations.restype = _i32
+_lib.hobf_quantize_activations.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _i32, _p, _p]
 _lib.hobf_lop3_peak.restype = _i32
 _lib.hobf_lop3_peak.argtypes = [_i32, _i32, _i32, _p, _p, ctypes.POINTER(_i64)]
 _lib.hobf_last_launch_count.restype = _i32
@@ -106,7 +108,7 @@ SYMBOLS = ["hobf_nbits", "hobf_out_wf", "hobf_nplanes", "hobf_planes_words", "ho
            "hobf_unpack", "hobf_unpack_f32", "hobf_conv2d", "hobf_mac_planes", "hobf_gate_count",
            "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version",
            "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_xrec_words",
-           "hobf_prepare_activations"]
+           "hobf_prepare_activations", "hobf_quantize_activations"]
 
 
 def _check(fn, st):
@@ -251,6 +253,17 @@ def prepare_activations(f: Fmt, x_planes: torch.Tensor, n: int, h: int, w: int, 
     return out
 
 
+def quantize_activations(f: Fmt, x: torch.Tensor, pad: int, out=None, stream=None) -> torch.Tensor:
+    """float32 NHWC [n,h,w,cin] (CUDA) -> records for conv2d_prepared, quantised with f.round."""
+    assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.dim() == 4
+    n, h, w, cin = x.shape
+    if out is None:
+        out = torch.empty(max(xrec_words(n, h, w, cin, pad), 1), dtype=torch.int32, device=x.device)
+    _check("hobf_quantize_activations", _lib.hobf_quantize_activations(f.c(), _ptr(x), n, h, w, cin, pad, _ptr(out),
+                                                                       _stream(stream)))
+    return out
+
+
 def conv2d_prepared(f: Fmt, xrec: torch.Tensor, n: int, h: int, w: int, cin: int, wtab: torch.Tensor,
                     kh: int, kw: int, cout: int, stride: int = 1, pad: int = 1, relu: int = 0, out=None,
                     stream=None) -> torch.Tensor:
@@ -297,8 +310,13 @@ class Conv2d:
     def __call__(self, x_f32: torch.Tensor) -> torch.Tensor:
         n, h, w, cin = x_f32.shape
         assert cin == self.cin
-        xp = quantize_pack(self.f.we, self.f.wf, x_f32.reshape(n * h * w, cin).contiguous(), self.f.round)
-        yp = self.forward_planes(xp, n, h, w)
+        if self.wtab is not None:
+            xrec = quantize_activations(self.f, x_f32.contiguous(), self.pad)
+            yp = conv2d_prepared(self.f, xrec, n, h, w, cin, self.wtab, self.kh, self.kw, self.cout, self.stride,
+                                 self.pad, int(self.relu))
+        else:
+            xp = quantize_pack(self.f.we, self.f.wf, x_f32.reshape(n * h * w, cin).contiguous(), self.f.round)
+            yp = self.forward_planes(xp, n, h, w)
         ho, wo = conv_out_hw(h, w, self.kh, self.kw, self.stride, self.pad)
         y = unpack_f32(self.f.we, self.f.wfo, yp, n * ho * wo, self.cout)
         return y.reshape(n, ho, wo, self.cout)

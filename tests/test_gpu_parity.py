@@ -332,3 +332,26 @@ def test_conv_public_api_float():
     y = layer(torch.from_numpy(x).cuda()).cpu().numpy()
     exp = oracle.decode_f64(oracle_conv(x, w, f, relu=1), 5, 11)
     assert np.array_equal(y.astype(np.float64), exp)
+
+
+@pytest.mark.parametrize("we,wf,pad", [(5, 3, 1), (4, 3, 0), (5, 10, 2), (6, 7, 1)])
+def test_activation_records_two_ways_agree(we, wf, pad):
+    """quantize_activations(float32) == prepare_activations(quantize_pack(float32)), and the
+    record's low bits are the oracle's encoding (padding = +0 with the zero row)."""
+    H = hobf()
+    rng = np.random.default_rng(we + wf + pad)
+    n, h, w, cin = 2, 9, 37, 40
+    x = (rng.standard_normal((n, h, w, cin)) * np.exp(rng.uniform(-8, 8, (n, h, w, cin)))).astype(np.float32)
+    x.ravel()[:20] = special_floats()[:20]
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd)
+        xt = torch.from_numpy(x).cuda()
+        r1 = to_np_words(H.quantize_activations(f, xt, pad))
+        xp = H.quantize_pack(we, wf, xt.reshape(-1, cin), rnd)
+        r2 = to_np_words(H.prepare_activations(f, xp, n, h, w, cin, pad))
+        assert np.array_equal(r1, r2)
+        rec = r1.reshape(n, cin, h + 2 * pad, w + 2 * pad)
+        inner = rec[:, :, pad:pad + h, pad:pad + w] & np.uint32((1 << 20) - 1)
+        assert np.array_equal(inner.transpose(0, 2, 3, 1), oracle.encode_f32(x, we, wf, rnd))
+        if pad:
+            assert np.all(rec[:, :, 0, :] == np.uint32((1 << wf) << 20))
