@@ -46,6 +46,7 @@ def parse_args(argv=None):
     ap.add_argument("--format", default=None, help="override format, e.g. e5m10")
     ap.add_argument("--round", default="rne", choices=["rne", "rtz"])
     ap.add_argument("--relu", type=int, default=0)
+    ap.add_argument("--extended", type=int, default=0, help="1 = extended MAC class (exact product, 2wF+1 accumulator)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "gates", "tables"],
                     help="conv kernel: gates = full lop3 MAC (hobf_conv2d); tables = prepared weights "
                          "(hobf_prepare_weights + hobf_conv2d_prepared); auto = tables when the format has them")
@@ -196,7 +197,7 @@ def run_reference(a, dist):
     return 0
 
 
-def cpu_baseline(cfg, we, wf, rnd, relu, target_macs):
+def cpu_baseline(cfg, we, wf, wfo, rnd, relu, target_macs):
     import oracle
     cores = os.cpu_count() or 1
     per_img = cfg.macs(1)
@@ -205,19 +206,19 @@ def cpu_baseline(cfg, we, wf, rnd, relu, target_macs):
     xq = oracle.encode_f32(x, we, wf, rnd)
     wq = oracle.encode_f32(w, we, wf, rnd)
     t0 = time.perf_counter()
-    oracle.conv2d(xq, wq, we, wf, wf + 1, rnd, cfg.stride, cfg.pad, relu, nthreads=cores)
+    oracle.conv2d(xq, wq, we, wf, wfo, rnd, cfg.stride, cfg.pad, relu, nthreads=cores)
     dt = time.perf_counter() - t0
     return {"value": cfg.macs(n) / dt, "unit": "MAC/s", "cores": cores, "kind": "oracle",
             "sample": f"{n} of {cfg.n} images of {cfg.name} (full conv, every output exact), {dt:.1f} s"}
 
 
-def parity_sample(cfg, we, wf, rnd, relu, y_words, x_f32, w_f32, k=256):
+def parity_sample(cfg, we, wf, wfo, rnd, relu, y_words, x_f32, w_f32, k=256):
     import oracle
     xq = oracle.encode_f32(x_f32, we, wf, rnd)
     wq = oracle.encode_f32(w_f32, we, wf, rnd)
     rng = np.random.default_rng(123)
     idx = rng.integers(0, y_words.size, k)
-    exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wf + 1, rnd, cfg.stride, cfg.pad, relu)
+    exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wfo, rnd, cfg.stride, cfg.pad, relu)
     return {"checked": int(k), "mismatches": int((y_words.ravel()[idx] != exp).sum())}
 
 
@@ -232,7 +233,7 @@ def run_gpu(a, dist):
     cfg = inputs.CONFIGS[a.config]
     we, wf = fmt_of(cfg, a.format)
     rnd = 0 if a.round == "rne" else 1
-    f = H.Fmt(we, wf, rnd)
+    f = H.Fmt(we, wf, rnd, extended=a.extended)
     n = cfg.n
     x_np, w_np = inputs.draw(cfg, n=n, shard=dist.rank)
     rows_x, rows_w, rows_y = n * cfg.h * cfg.w, cfg.kh * cfg.kw * cfg.cin, n * cfg.ho * cfg.wo
@@ -376,9 +377,9 @@ def run_gpu(a, dist):
     line = {
         "metric": METRIC, "value": value, "unit": "MAC/s", "n_gpus": dist.world, "steps": K, "warmup": a.warmup,
         "ms_per_step": t_max / K * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": f"e{we}m{wf}->e{we}m{wf + 1} custom FP, bitsliced u32 lop3", "data": "synthetic",
+        "dtype": f"e{we}m{wf}->e{we}m{f.wfo} custom FP, bitsliced u32 lop3", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.text}", "format": f"e{we}m{wf}", "round": a.round,
-                   "relu": a.relu, "global_batch": n * dist.world, "per_gpu_batch": n,
+                   "mac_class": "extended" if a.extended else "single", "relu": a.relu, "global_batch": n * dist.world, "per_gpu_batch": n,
                    "dense_macs_per_step": macs_rank * dist.world, "l2": "flushed (256 MiB write) between timed steps",
                    "step": ("quantize_activations(x) + quantize_pack(w) + prepare_weights + conv2d_prepared + unpack_f32(y)"
                             if use_tab else "quantize_pack(x) + quantize_pack(w) + conv2d + unpack_f32(y)"),
@@ -397,9 +398,9 @@ def run_gpu(a, dist):
         "clocks": clk,
     }
     if dist.world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, we, wf, rnd, a.relu, a.cpu_sample_macs)
+        line["cpu_baseline"] = cpu_baseline(cfg, we, wf, f.wfo, rnd, a.relu, a.cpu_sample_macs)
         yw = H.unpack(we, f.wfo, yps[0], rows_y, cfg.cout).cpu().numpy().view(np.uint32)
-        line["parity_sample"] = parity_sample(cfg, we, wf, rnd, a.relu, yw, x_np, w_np)
+        line["parity_sample"] = parity_sample(cfg, we, wf, f.wfo, rnd, a.relu, yw, x_np, w_np)
     print(json.dumps(line), flush=True)
     return 0
 

@@ -56,8 +56,11 @@ typedef enum {
 
 typedef enum { HOBF_RNE = 0, HOBF_RTZ = 1 } hobf_round;
 
-/* Input format + MAC mode.  extended: 0 = single class (wF+1), 1 = extended
- * (2wF+1; not yet implemented on the GPU -> HOBF_EUNSUPPORTED). */
+/* Input format + MAC mode.  extended: 0 = single class (product and
+ * accumulator fraction wF+1, rounded with `round`); 1 = extended class
+ * (HOBFLOPSxxe: the product is exact at 2wF+1 fraction bits,
+ * the accumulator is 2wF+1 bits wide and the adder rounds with `round`; RTZ is
+ * the paper's cheaper adder).  Outputs are in F(we, hobf_out_wf(f)). */
 typedef struct {
   int32_t we, wf, round, extended;
 } hobf_fmt;

@@ -19,8 +19,8 @@ using hobf::FormatEntry;
   cudaError_t hobf_launch_mac_##TAG(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n, \
                                     cudaStream_t s);                                         \
   cudaError_t hobf_launch_convtab_##TAG(const hobf::ConvArgs& a, cudaStream_t s);
-#define HOBF_ENTRY(TAG, WE, WF, RND, GM, GMUL, GADD, GRELU, GTAB) \
-  {WE, WF, RND, GM, GMUL, GADD, GRELU, GTAB, hobf_launch_conv_##TAG, hobf_launch_mac_##TAG, hobf_launch_convtab_##TAG},
+#define HOBF_ENTRY(TAG, WE, WF, RND, EXT, GM, GMUL, GADD, GRELU, GTAB) \
+  {WE, WF, RND, EXT, GM, GMUL, GADD, GRELU, GTAB, hobf_launch_conv_##TAG, hobf_launch_mac_##TAG, hobf_launch_convtab_##TAG},
 #include "gen/hobf_table.inc"
 
 static const FormatEntry kFormats[] = {HOBF_TABLE_ENTRIES};
@@ -28,9 +28,10 @@ static const int kNumFormats = (int)(sizeof(kFormats) / sizeof(kFormats[0]));
 
 static thread_local int32_t g_last_launches = 0;
 
-static const FormatEntry* find_format(int we, int wf, int rnd) {
+static const FormatEntry* find_format(int we, int wf, int rnd, int ext) {
   for (int i = 0; i < kNumFormats; i++)
-    if (kFormats[i].we == we && kFormats[i].wf == wf && kFormats[i].rnd == rnd) return &kFormats[i];
+    if (kFormats[i].we == we && kFormats[i].wf == wf && kFormats[i].rnd == rnd && kFormats[i].ext == ext)
+      return &kFormats[i];
   return nullptr;
 }
 
@@ -172,7 +173,8 @@ static unsigned warp_grid(int64_t items) {
 // Largest wF with a prepared-weights (table) kernel; the table has 2^wF + 3 rows.
 static const int kTabMaxWf = 10;
 
-__host__ __device__ static inline int tab_width(int we, int wf) { return (wf + 1) + (we + 2) + 3; }
+// entry planes: product fraction (wfo = wF+1, or 2wF+1 extended) | Epart (wE+2) | S | K0 | K1
+__host__ __device__ static inline int tab_width(int we, int wfo) { return wfo + (we + 2) + 3; }
 __host__ __device__ static inline int tab_rows(int wf) { return (1 << wf) + 3; }
 
 // One table entry for weight word w (canonical) and table row r (see
@@ -185,8 +187,9 @@ __host__ __device__ static inline int tab_rows(int wf) { return (1 << wf) + 3; }
 //   bits wF+wE+4, +5       product class K0, K1 (00 zero, 01 normal, 10 inf,
 //                          11 NaN), exception algebra of S:68 / SURVEY 8(c) mul
 // Rows: r < 2^wF: normal x with fraction r; 2^wF: x zero; +1: x inf; +2: x NaN.
-__device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int rnd) {
-  const int wfo = wf + 1, EW = we + 2;
+// Extended class (wfo = 2wF+1): the product fraction is exact (no rounding).
+__device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int wfo, int rnd) {
+  const int EW = we + 2;
   const uint32_t exc = (w >> (wf + we + 1)) & 3u;
   const uint32_t sw = (w >> (wf + we)) & 1u;
   const uint32_t eb = (w >> wf) & ((1u << we) - 1u);
@@ -207,10 +210,13 @@ __device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int rnd) {
   const uint32_t P = ma * mb;  // < 2^(2wf+2) <= 2^22 for wf <= 10
   const uint32_t top = (P >> (2 * wf + 1)) & 1u;
   const uint32_t N = top ? P : (P << 1);       // leading one at bit 2wf+1
-  uint32_t kept = N >> wf;                     // wfo+1 bits
-  const uint32_t rem = N & ((1u << wf) - 1u);  // below the kept bits
-  const uint32_t half = 1u << (wf - 1);
-  if (rnd == 0 && (rem > half || (rem == half && (kept & 1u)))) kept += 1u;
+  const int sh = 2 * wf + 1 - wfo;             // bits below the kept wfo+1 (0 if extended)
+  uint32_t kept = N >> sh;
+  if (sh > 0) {
+    const uint32_t rem = N & ((1u << sh) - 1u);
+    const uint32_t half = 1u << (sh - 1);
+    if (rnd == 0 && (rem > half || (rem == half && (kept & 1u)))) kept += 1u;
+  }
   uint32_t inc = top;
   if (kept == (2u << wfo)) { kept >>= 1; inc += 1u; }
   const uint32_t frac = kept - (1u << wfo);
@@ -298,11 +304,12 @@ __global__ void __launch_bounds__(256) quantize_acts_kernel(const float* __restr
 // its weight from the planes (shfl transpose), computes its entry, and the
 // entry bits are ballot-transposed back into NPT planes.
 __global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restrict__ wplanes, int64_t wrows, int G,
-                                                         int we, int wf, int rnd, uint32_t* __restrict__ wtab) {
+                                                         int we, int wf, int wfo, int rnd,
+                                                         uint32_t* __restrict__ wtab) {
   const int lane = threadIdx.x & 31;
   const int npi = (3 + we + wf + 3) / 4 * 4;
   const int rows = tab_rows(wf);
-  const int npt = (tab_width(we, wf) + 3) / 4 * 4;
+  const int npt = (tab_width(we, wfo) + 3) / 4 * 4;
   const int64_t items = wrows * G * rows;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restr
     const uint32_t mine = lane < npi ? __ldg(wplanes + grp * npi + lane) : 0u;
     uint32_t w = 0u;
     for (int j = 0; j < 3 + we + wf; j++) w |= ((__shfl_sync(0xffffffffu, mine, j) >> lane) & 1u) << j;
-    const uint32_t e = tab_entry(w, r, we, wf, rnd);
+    const uint32_t e = tab_entry(w, r, we, wf, wfo, rnd);
     uint32_t out = 0u;
     for (int j = 0; j < npt; j++) {
       const uint32_t bal = __ballot_sync(0xffffffffu, (e >> j) & 1u);
@@ -443,7 +450,7 @@ hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32
   if (h == 0 || w == 0 || cin == 0 || kh == 0 || kw == 0 || cout == 0) return HOBF_ESHAPE;
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
   if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
-  const FormatEntry* e = f.extended ? nullptr : find_format(f.we, f.wf, f.round);
+  const FormatEntry* e = find_format(f.we, f.wf, f.round, f.extended);
   if (!e) return HOBF_EUNSUPPORTED;
   if (n == 0) return HOBF_OK;
   if (!d_x_planes || !d_w_planes || !d_y_planes) return HOBF_EINVAL;
@@ -465,7 +472,7 @@ hobf_status hobf_mac_planes(hobf_fmt f, uint32_t* d_acc, const uint32_t* d_a, co
                             hobf_stream stream) {
   g_last_launches = 0;
   if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || n_groups < 0) return HOBF_EINVAL;
-  const FormatEntry* e = f.extended ? nullptr : find_format(f.we, f.wf, f.round);
+  const FormatEntry* e = find_format(f.we, f.wf, f.round, f.extended);
   if (!e) return HOBF_EUNSUPPORTED;
   if (n_groups == 0) return HOBF_OK;
   if (!d_acc || !d_a || !d_b || !aligned16(d_acc) || !aligned16(d_a) || !aligned16(d_b)) return HOBF_EINVAL;
@@ -476,7 +483,7 @@ hobf_status hobf_mac_planes(hobf_fmt f, uint32_t* d_acc, const uint32_t* d_a, co
 
 hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add, int32_t* relu,
                             int32_t* mac_tab) {
-  const FormatEntry* e = f.extended ? nullptr : find_format(f.we, f.wf, f.round);
+  const FormatEntry* e = find_format(f.we, f.wf, f.round, f.extended);
   if (!e) return HOBF_EUNSUPPORTED;
   if (mac) *mac = e->g_mac;
   if (mul) *mul = e->g_mul;
@@ -497,14 +504,14 @@ static int conv_tab_variant() {
 }
 
 static const FormatEntry* tab_format(hobf_fmt f) {
-  if (f.extended || f.wf > kTabMaxWf) return nullptr;
-  return find_format(f.we, f.wf, f.round);
+  if (f.wf > kTabMaxWf) return nullptr;
+  return find_format(f.we, f.wf, f.round, f.extended);
 }
 
 int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t cout) {
   if (!fmt_ok(f.we, f.wf) || kh <= 0 || kw <= 0 || cin <= 0 || cout <= 0) return -1;
   if (!tab_format(f)) return -1;
-  const int64_t npt = (tab_width(f.we, f.wf) + 3) / 4 * 4;
+  const int64_t npt = (tab_width(f.we, hobf_out_wf(f)) + 3) / 4 * 4;
   return (int64_t)kh * kw * cin * ((cout + 31) / 32) * tab_rows(f.wf) * npt;
 }
 
@@ -519,8 +526,8 @@ hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t
   const int G = (cout + 31) / 32;
   const int64_t wrows = (int64_t)kh * kw * cin;
   const int64_t items = wrows * G * tab_rows(f.wf);
-  build_wtab_kernel<<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(d_w_planes, wrows, G, f.we, f.wf, f.round,
-                                                                          d_wtab);
+  build_wtab_kernel<<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(d_w_planes, wrows, G, f.we, f.wf,
+                                                                          hobf_out_wf(f), f.round, d_wtab);
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;

@@ -22,7 +22,7 @@ typedef cudaError_t (*conv_launcher)(const ConvArgs&, cudaStream_t);
 typedef cudaError_t (*mac_launcher)(uint32_t*, const uint32_t*, const uint32_t*, int64_t, cudaStream_t);
 
 struct FormatEntry {
-  int we, wf, rnd, g_mac, g_mul, g_add, g_relu, g_tab;
+  int we, wf, rnd, ext, g_mac, g_mul, g_add, g_relu, g_tab;
   conv_launcher conv;
   mac_launcher mac;
   conv_launcher conv_tab;  // conv with the multiplier read from per-weight tables

@@ -280,18 +280,12 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     const int64_t warps = (npix + 31) / 32 * gy;
     variant = (F::WF >= 8 || warps < 148 * 4 * 4) ? 4 : 3;
   }
-  switch (variant) {
-    case 1: conv_tab_kernel<F, 128, 1, false, false><<<grid(128), 128, 0, s>>>(a); break;
-    case 3:
-      if (k3) conv_tab_kernel<F, 128, 9, true, false><<<grid(128), 128, 0, s>>>(a);
-      else conv_tab_kernel<F, 128, 9, false, false><<<grid(128), 128, 0, s>>>(a);
-      break;
-    case 4:  // pipelined (latency-bound configs)
-      if (k3) conv_tab_kernel<F, 128, 1, true, true><<<grid(128), 128, 0, s>>>(a);
-      else conv_tab_kernel<F, 128, 1, false, true><<<grid(128), 128, 0, s>>>(a);
-      break;
-    case 5: conv_tab_kernel<F, 64, 1, false, true><<<grid(64), 64, 0, s>>>(a); break;
-    default: conv_tab_kernel<F, 128, 9, false, false><<<grid(128), 128, 0, s>>>(a); break;
+  if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
+    conv_tab_kernel<F, 128, 1, false, true><<<grid(128), 128, 0, s>>>(a);
+  } else if (k3) {     // kernel width 3 unrolled, <= 56 registers (9 CTAs / SM)
+    conv_tab_kernel<F, 128, 9, true, false><<<grid(128), 128, 0, s>>>(a);
+  } else {
+    conv_tab_kernel<F, 128, 9, false, false><<<grid(128), 128, 0, s>>>(a);
   }
   return cudaGetLastError();
 }

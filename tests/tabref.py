@@ -19,10 +19,12 @@ def row_of(x, we, wf):
     return np.where(exc == 1, fa, (1 << wf) + special)
 
 
-def entries(w, r, we, wf, rnd):
+def entries(w, r, we, wf, rnd, wfo=None):
+    """wfo = wF+1 (single class, rounded) or 2wF+1 (extended class, exact)."""
     w = np.asarray(w, dtype=np.int64)
     r = np.asarray(r, dtype=np.int64)
-    wfo, EW = wf + 1, we + 2
+    wfo = wf + 1 if wfo is None else wfo
+    EW = we + 2
     exc = (w >> (wf + we + 1)) & 3
     sw = (w >> (wf + we)) & 1
     eb = (w >> wf) & ((1 << we) - 1)
@@ -38,10 +40,11 @@ def entries(w, r, we, wf, rnd):
     P = ma * mb
     top = (P >> (2 * wf + 1)) & 1
     N = np.where(top == 1, P, P << 1)
-    kept = N >> wf
-    rem = N & ((1 << wf) - 1)
-    half = 1 << (wf - 1)
-    if rnd == 0:
+    sh = 2 * wf + 1 - wfo
+    kept = N >> sh
+    if sh > 0 and rnd == 0:
+        rem = N & ((1 << sh) - 1)
+        half = 1 << (sh - 1)
         kept = kept + ((rem > half) | ((rem == half) & ((kept & 1) == 1)))
     inc = top.copy()
     carry = kept == (2 << wfo)
@@ -58,10 +61,10 @@ def entries(w, r, we, wf, rnd):
     return out.astype(np.uint32)
 
 
-def circuit_inputs(acc, x, w, we, wf, rnd):
+def circuit_inputs(acc, x, w, we, wf, rnd, wfo=None):
     """Arrays for build_mac_tab's inputs (acc, t, ea, sx) for lane-wise (acc, x, w)."""
     x = np.asarray(x, dtype=np.int64)
-    t = entries(w, row_of(x, we, wf), we, wf, rnd)
+    t = entries(w, row_of(x, we, wf), we, wf, rnd, wfo)
     ea = ((x >> wf) & ((1 << we) - 1)).astype(np.uint32)
     sx = ((x >> (wf + we)) & 1).astype(np.uint32)
     return [np.asarray(acc, np.uint32), t, ea, sx]

@@ -225,3 +225,36 @@ def test_mac_tab_random(we, wf, rnd):
     p = oracle.mul(x[:half], w[:half], we, wf, wf + 1, rnd)
     acc[:half] = np.where(rng.random(half) < 0.5, p ^ np.uint32(1 << (wf + 1 + we)), acc[:half])
     _check(c, m, tabref.circuit_inputs(acc, x, w, we, wf, rnd), oracle.mac(acc, x, w, we, wf, wf + 1, rnd))
+
+
+# ----------------------------------------------------------------------------- extended class
+
+@pytest.mark.parametrize("we,wf", [(5, 2), (4, 3), (5, 3)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_extended_mul_exhaustive(we, wf, rnd):
+    """HOBFLOPSxxe multiplier: exact product at 2wF+1 (only over/underflow can differ from exact)."""
+    c = fpgen.build_mul(we, wf, 2 * wf + 1, rnd)
+    m = lutmap.map_aig(c.g, c.outputs)
+    w = canon_words(we, wf)
+    A, B = np.meshgrid(w, w, indexing="ij")
+    A, B = A.ravel(), B.ravel()
+    _check(c, m, [A, B], oracle.mul(A, B, we, wf, 2 * wf + 1, rnd))
+
+
+@pytest.mark.parametrize("we,wf", [(5, 2), (4, 3), (5, 10), (6, 5)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_extended_mac_and_mac_tab_random(we, wf, rnd):
+    wfo = 2 * wf + 1
+    rng = np.random.default_rng(we * 7 + wf + 100 * rnd)
+    N = 100_000
+    acc = _rand_words(rng, N, we, wfo)
+    x = _rand_words(rng, N, we, wf)
+    w = _rand_words(rng, N, we, wf)
+    half = N // 2
+    p = oracle.mul(x[:half], w[:half], we, wf, wfo, rnd)
+    acc[:half] = np.where(rng.random(half) < 0.5, p ^ np.uint32(1 << (wfo + we)), acc[:half])
+    exp = oracle.mac(acc, x, w, we, wf, wfo, rnd)
+    c = fpgen.build_mac(we, wf, wfo, rnd)
+    _check(c, lutmap.map_aig(c.g, c.outputs), [acc, x, w], exp)
+    ct = fpgen.build_mac_tab(we, wf, rnd, wfo)
+    _check(ct, lutmap.map_aig(ct.g, ct.outputs), tabref.circuit_inputs(acc, x, w, we, wf, rnd, wfo), exp)

@@ -86,7 +86,7 @@ def test_empty_and_error_paths():
         H.gate_count(H.Fmt(7, 3))
     assert e.value.status == 3
     with pytest.raises(H.HobfError) as e:
-        H.conv2d(H.Fmt(5, 3, extended=1), torch.zeros(64, dtype=torch.int32, device="cuda"), 1, 2, 2, 1,
+        H.conv2d(H.Fmt(7, 3, extended=1), torch.zeros(64, dtype=torch.int32, device="cuda"), 1, 2, 2, 1,
                  torch.zeros(64, dtype=torch.int32, device="cuda"), 3, 3, 1)
     assert e.value.status == 3
     with pytest.raises(H.HobfError) as e:  # kernel larger than padded input
@@ -186,6 +186,8 @@ def test_gate_counts_reported():
             g = H.gate_count(H.Fmt(we, wf, rnd))
             assert g["mac"] == counts[f"e{we}m{wf}_{name}"]["g_mac"]
             assert g["mac_tab"] == counts[f"e{we}m{wf}_{name}"]["g_tab"]
+            gx = H.gate_count(H.Fmt(we, wf, rnd, extended=1))
+            assert gx["mac_tab"] == counts[f"e{we}m{wf}x_{name}"]["g_tab"]
 
 
 # ----------------------------------------------------------------------------- conv
@@ -355,3 +357,40 @@ def test_activation_records_two_ways_agree(we, wf, pad):
         assert np.array_equal(inner.transpose(0, 2, 3, 1), oracle.encode_f32(x, we, wf, rnd))
         if pad:
             assert np.all(rec[:, :, 0, :] == np.uint32((1 << wf) << 20))
+
+
+
+# ----------------------------------------------------------------------------- extended class
+
+@pytest.mark.parametrize("we,wf", [(5, 2), (5, 3), (4, 3), (5, 10), (6, 6)])
+@pytest.mark.parametrize("prepared", [False, True])
+def test_conv_extended_class(we, wf, prepared):
+    """HOBFLOPSxxe: exact products, accumulator at 2wF+1, both rounding modes."""
+    H = hobf()
+    x, wt = inputs.small_case(we * 10 + wf, 2, 7, 9, 40, 40, "normal", 0.5)
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd, extended=1)
+        assert f.wfo == 2 * wf + 1
+        got = gpu_conv(x, wt, f, 1, 1, rnd, prepared=prepared)
+        exp = oracle_conv(x, wt, f, 1, 1, rnd)
+        assert np.array_equal(got, exp), np.argwhere(got != exp)[:5]
+
+
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 7), (6, 10)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_mac_random_extended(we, wf, rnd):
+    H = hobf()
+    f = H.Fmt(we, wf, rnd, extended=1)
+    rng = np.random.default_rng(we * 31 + wf * 3 + rnd)
+    N = 1 << 16
+
+    def rw(wfx):
+        s = rng.integers(0, 2, N)
+        e = rng.integers(0, 1 << we, N)
+        fr = rng.integers(0, 1 << wfx, N)
+        return ((1 << (wfx + we + 1)) | (s << (wfx + we)) | (e << wfx) | fr).astype(np.uint32)
+
+    A, X, W = rw(f.wfo), rw(wf), rw(wf)
+    got = run_mac(f, A, X, W)
+    exp = oracle.mac(A, X, W, we, wf, f.wfo, rnd)
+    assert np.array_equal(got, exp)
