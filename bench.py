@@ -173,7 +173,8 @@ def run_reference(a, dist):
     sample_macs = ho_s * cfg.wo * cfg.cout * cfg.cin * cfg.kh * cfg.kw
 
     def step():
-        y = oracle.conv2d(xin, wq, we, wf, wf + 1, rnd, cfg.stride, cfg.pad, a.relu, nthreads=cores)
+        wfo = 2 * wf + 1 if a.extended else wf + 1
+        y = oracle.conv2d(xin, wq, we, wf, wfo, rnd, cfg.stride, cfg.pad, a.relu, nthreads=cores)
         return y
 
     for _ in range(a.warmup):

@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
       F::mac_tab(acc, cur.T, cur.EA, cur.SX);
     }
   }
+  F::canon(acc, acc);  // the chain keeps a relaxed accumulator (fpgen.build_mac_tab)
   if (a.relu) F::relu(acc, acc);
   uint4* py = reinterpret_cast<uint4*>(a.y + (pix * G + g) * F::NPO);
 #pragma unroll

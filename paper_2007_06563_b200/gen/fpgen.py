@@ -161,6 +161,25 @@ def lzc(g: AIG, v):
     return cnt, z
 
 
+def normalize_left(g: AIG, v):
+    """Leading-zero normalisation by successive detection: for 2^j from the
+    largest power of two down, if the top 2^j bits of the current vector are
+    all zero, shift it left by 2^j.  Returns (normalised v, shift count bits
+    LSB first, all_zero).  Same result as lzc + shift_left, fewer gates."""
+    L = len(v)
+    K = 0
+    while (1 << K) < L:
+        K += 1
+    cur = list(v)
+    cnt = [FALSE] * K
+    for j in reversed(range(K)):
+        sh = 1 << j
+        zj = g.NOT(g.OR_many(cur[L - sh:]))
+        cnt[j] = zj
+        cur = [g.MUX(zj, cur[i - sh] if i - sh >= 0 else FALSE, cur[i]) for i in range(L)]
+    return cur, cnt, g.NOT(cur[L - 1])
+
+
 def shift_left(g: AIG, v, s):
     cur = list(v)
     W = len(v)
@@ -247,12 +266,12 @@ class Operand:
         self.canonical = canonical
 
     @staticmethod
-    def from_word(g: AIG, A: FP):
+    def from_word(g: AIG, A: FP, canonical: bool = True):
         nan = g.AND(A.exc1, A.exc0)
         inf = g.AND(A.exc1, g.NOT(A.exc0))
         norm = g.AND(g.NOT(A.exc1), A.exc0)
         zero = g.AND(g.NOT(A.exc1), g.NOT(A.exc0))
-        return Operand(A.we, A.wf, A.frac, A.exp, A.sign, norm, zero, inf, nan, A.exc1, True)
+        return Operand(A.we, A.wf, A.frac, A.exp, A.sign, norm, zero, inf, nan, A.exc1, canonical)
 
 
 def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
@@ -260,7 +279,8 @@ def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
     return fp_add_ops(g, Operand.from_word(g, A), Operand.from_word(g, B), rnd, shift_order)
 
 
-def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_first"):
+def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_first", norm="detect",
+               expo="one_adder", canon_out=True):
     """HOBFLOPS adder F(wE,w) + F(wE,w) -> F(wE,w) (single-path, P:190-198;
     SURVEY 8(c) add; ledger L5-L7).  A must be canonical; B may be
     non-canonical (its exp/frac are ignored when it is zero or special).
@@ -284,7 +304,11 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
     keyA = [hA] + list(A.frac) + list(A.exp)
     keyB = [hB] + list(B.frac) + list(B.exp)
     lt = less_than(g, keyA, keyB)
-    swap = lt if B.canonical else g.AND(lt, g.NOT(B.zero))
+    swap = lt
+    if not A.canonical:      # a zero A (arbitrary exp/frac) always goes to Y
+        swap = g.OR(swap, A.zero)
+    if not B.canonical:      # a zero B (arbitrary exp/frac) never goes to X
+        swap = g.AND(swap, g.NOT(B.zero))
     eX = [g.MUX(swap, b, a) for a, b in zip(A.exp, B.exp)]
     eY = [g.MUX(swap, a, b) for a, b in zip(A.exp, B.exp)]
     fX = [g.MUX(swap, b, a) for a, b in zip(A.frac, B.frac)]
@@ -294,6 +318,9 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
     sX = g.MUX(swap, B.sign, A.sign)
     sub = g.XOR(A.sign, B.sign)
     kill = FALSE if B.canonical else g.AND(g.NOT(swap), B.zero)
+    if not A.canonical:
+        kill = g.OR(kill, g.AND(swap, A.zero))
+    both_zero = FALSE if A.canonical else g.AND(A.zero, B.zero)
 
     # d = eX - eY >= 0
     d = ripple_add(g, eX, [g.NOT(x) for x in eY], TRUE, width=we)
@@ -307,9 +334,12 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
     yo = [g.XOR(ys, sub)] + [g.XOR(b, sub) for b in yv]
     Z = ripple_add(g, xo, yo, sub, width=W + 2)  # Z[W+1] = carry (add) / discard (sub)
     Z[W + 1] = g.AND(Z[W + 1], g.NOT(sub))
-    # normalise: leading-zero count over Z[W+1..0]
-    cnt, zsum = lzc(g, Z)
-    Zn = shift_left(g, Z, cnt)
+    # normalise: leading-zero count over Z[W+1..0] and left shift
+    if norm == "detect":
+        Zn, cnt, zsum = normalize_left(g, Z)
+    else:
+        cnt, zsum = lzc(g, Z)
+        Zn = shift_left(g, Z, cnt)
     # kept p bits: Zn[W+1 .. W+2-p] = Zn[p+3 .. 4]; guard Zn[3]; sticky Zn[2..0]
     kept = Zn[4:p + 4]
     guard = Zn[3]
@@ -323,23 +353,41 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
     # exponent: eX + 1 - cnt + rc  (wE+2 bits two's complement)
     EW = we + 2
     ncnt = [g.NOT(c) for c in cnt] + [TRUE] * (EW - len(cnt))  # ~cnt sign-extended
-    t = ripple_add(g, eX, ncnt, TRUE, width=EW)                # eX - cnt
-    E = ripple_add(g, t, const_bits(1, EW), rc, width=EW)
+    if expo == "one_adder":
+        k = ripple_add(g, ncnt, const_bits(2, EW), FALSE, width=EW)  # 1 - cnt = ~cnt + 2
+        E = ripple_add(g, eX, k, rc, width=EW)
+    else:
+        t = ripple_add(g, eX, ncnt, TRUE, width=EW)                # eX - cnt
+        E = ripple_add(g, t, const_bits(1, EW), rc, width=EW)
     unf = E[EW - 1]
     ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])
 
     nan = g.OR_many([A.nan, B.nan, g.AND(g.AND(A.inf, B.inf), sub)])
+    zsum = g.OR(zsum, both_zero)   # with a non-canonical A the datapath is garbage when both are zero
     fin_nz = g.AND(g.NOT(special), g.NOT(zsum))
     normal = g.AND(fin_nz, g.AND(g.NOT(ovf), g.NOT(unf)))
     exc1 = g.OR(special, g.AND(fin_nz, ovf))
     exc0 = g.OR(nan, normal)
-    zero_sign = g.AND(g.AND(A.sign, B.sign), g.NOT(hA))
+    # zero result: -0 only for (-0) + (-0); exact cancellation of normals gives +0 (L7)
+    zero_sign = g.AND(g.AND(A.sign, B.sign), A.zero if not A.canonical else g.NOT(hA))
     inf_sign = g.MUX(A.inf, A.sign, B.sign)
     sign_fin = g.MUX(zsum, zero_sign, sX)
     sign = g.AND(g.NOT(nan), g.MUX(special, inf_sign, sign_fin))
-    exp_out = [g.AND(normal, e) for e in E[:we]]
-    frac_out = [g.AND(normal, f) for f in frac]
+    if canon_out:
+        exp_out = [g.AND(normal, e) for e in E[:we]]
+        frac_out = [g.AND(normal, f) for f in frac]
+    else:           # exp/frac arbitrary unless normal (the next MAC reads A non-canonically)
+        exp_out, frac_out = E[:we], frac
     return pack_bits(frac_out, exp_out, sign, exc0, exc1)
+
+
+def fp_canon(g: AIG, A: FP):
+    """Canonical form of a word whose exp/frac are arbitrary unless normal
+    (S:38): exc != 01 -> exp = frac = 0; NaN sign 0."""
+    norm = g.AND(g.NOT(A.exc1), A.exc0)
+    nan = g.AND(A.exc1, A.exc0)
+    return pack_bits([g.AND(norm, f) for f in A.frac], [g.AND(norm, e) for e in A.exp],
+                     g.AND(A.sign, g.NOT(nan)), A.exc0, A.exc1)
 
 
 def fp_relu(g: AIG, A: FP):
@@ -392,6 +440,12 @@ def build_mac(we, wf, wfo, rnd, **kw) -> Circuit:
                    [("acc", 3 + we + wfo), ("x", 3 + we + wf), ("w", 3 + we + wf)], out)
 
 
+def build_canon(we, w) -> Circuit:
+    g = AIG()
+    a = g.inputs("a", 3 + we + w)
+    return Circuit(f"canon_e{we}m{w}", g, [("a", 3 + we + w)], fp_canon(g, FP(a, we, w)))
+
+
 def build_relu(we, w) -> Circuit:
     g = AIG()
     a = g.inputs("a", 3 + we + w)
@@ -442,16 +496,23 @@ def product_from_table(g: AIG, t, ea, sx, we: int, wf: int, wfo: int | None = No
     return Operand(we, wfo, F, E[:we], sign, norm, zero, inf, nan, special, canonical=False)
 
 
-def build_mac_tab(we, wf, rnd, wfo=None, **kw) -> Circuit:
+def build_mac_tab(we, wf, rnd, wfo=None, chained=True, **kw) -> Circuit:
     """acc' = add(acc, mul(x, w)) with the multiplier read from the weight table;
-    wfo = wF+1 (single class, default) or 2wF+1 (extended class)."""
+    wfo = wF+1 (single class, default) or 2wF+1 (extended class).
+
+    chained=True: the accumulator is read and written in a relaxed form whose
+    exp/frac bits are arbitrary unless it is normal (the class bits are exact);
+    the conv canonicalises once after the reduction (build_canon).  This saves
+    the per-MAC zeroing of the result fields."""
     wfo = wf + 1 if wfo is None else wfo
+    if chained:
+        kw.setdefault("canon_out", False)
     g = AIG()
     acc = g.inputs("acc", 3 + we + wfo)
     t = g.inputs("t", tab_entry_width(we, wf, wfo))
     ea = g.inputs("ea", we)
     sx = g.inputs("sx", 1)[0]
     B = product_from_table(g, t, ea, sx, we, wf, wfo)
-    out = fp_add_ops(g, Operand.from_word(g, FP(acc, we, wfo)), B, rnd, **kw)
+    out = fp_add_ops(g, Operand.from_word(g, FP(acc, we, wfo), canonical=not chained), B, rnd, **kw)
     return Circuit(f"mactab_e{we}m{wf}_o{wfo}_{'rne' if rnd == RNE else 'rtz'}", g,
                    [("acc", 3 + we + wfo), ("t", tab_entry_width(we, wf, wfo)), ("ea", we), ("sx", 1)], out)

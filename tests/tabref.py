@@ -68,3 +68,20 @@ def circuit_inputs(acc, x, w, we, wf, rnd, wfo=None):
     ea = ((x >> wf) & ((1 << we) - 1)).astype(np.uint32)
     sx = ((x >> (wf + we)) & 1).astype(np.uint32)
     return [np.asarray(acc, np.uint32), t, ea, sx]
+
+
+def canon(words, we, wf):
+    """Canonical form: exc != 01 -> exp = frac = 0; NaN -> sign 0."""
+    v = np.asarray(words, dtype=np.int64)
+    exc = (v >> (wf + we + 1)) & 3
+    v = np.where(exc != 1, v & ~((1 << (wf + we)) - 1), v)
+    v = np.where(exc == 3, v & ~(1 << (wf + we)), v)
+    return v.astype(np.uint32)
+
+
+def relax(words, we, wf, rng):
+    """Scramble exp/frac of non-normal words (the chained accumulator's relaxed form)."""
+    v = np.asarray(words, dtype=np.int64)
+    exc = (v >> (wf + we + 1)) & 3
+    junk = rng.integers(0, 1 << (wf + we), v.size)
+    return np.where(exc != 1, v | junk, v).astype(np.uint32)

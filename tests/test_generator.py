@@ -65,10 +65,12 @@ def test_lop3_truth_table_convention():
 
 # ----------------------------------------------------------------------------- circuits vs oracle
 
-def _check(circuit, mapping, arrays, expected):
-    got_aig = bitsim.run_aig(circuit, arrays)
+def _check(circuit, mapping, arrays, expected, post=None):
+    """post: applied to the circuit outputs before comparing (e.g. canonicalisation)."""
+    post = post or (lambda v: v)
+    got_aig = post(bitsim.run_aig(circuit, arrays))
     assert np.array_equal(got_aig, expected), "AIG differs from oracle"
-    got_map = bitsim.run_mapping(circuit, mapping, arrays)
+    got_map = post(bitsim.run_mapping(circuit, mapping, arrays))
     assert np.array_equal(got_map, expected), "LOP3 mapping differs from oracle"
 
 
@@ -178,12 +180,31 @@ def test_emitted_headers_up_to_date(tmp_path):
     for name in ["hobf_circuit_e5m3_rne.cuh", "hobf_circuit_e4m10_rtz.cuh", "hobf_fmt_e5m3.cu"]:
         assert open(os.path.join(gen_dir, name)).read() == open(os.path.join(tmp_path, name)).read(), name
     counts = json.load(open(os.path.join(gen_dir, "gate_counts.json")))
-    assert len(counts) == 54
+    assert len(counts) == 108  # 27 formats x {RNE, RTZ} x {single, extended}
 
 
 def test_emitted_mac_lop3_count_matches_mapping():
     r = emit.gen_format(5, 3, 0)
-    assert r["src"].count("hobf_lop3<") == r["g_mac"] + r["g_relu"]
+    n_canon = lutmap.map_aig(fpgen.build_canon(5, 4).g, fpgen.build_canon(5, 4).outputs).n_luts
+    assert r["src"].count("hobf_lop3<") == r["g_mac"] + r["g_tab"] + r["g_relu"] + n_canon
+
+
+def test_chained_relaxed_accumulator_over_many_steps():
+    """A chain of MACs through the relaxed accumulator, canonicalised at the end,
+    equals the oracle's chain step for step."""
+    we, wf = 5, 3
+    c = fpgen.build_mac_tab(we, wf, 0)
+    m = lutmap.map_aig(c.g, c.outputs)
+    rng = np.random.default_rng(0)
+    xi = canon_words(we, wf)
+    N = 100_000
+    acc = np.zeros(N, np.uint32)
+    ref = acc.copy()
+    for _ in range(8):
+        x, w = rng.choice(xi, N), rng.choice(xi, N)
+        acc = bitsim.run_mapping(c, m, tabref.circuit_inputs(acc, x, w, we, wf, 0))
+        ref = oracle.mac(ref, x, w, we, wf, wf + 1, 0)
+        assert np.array_equal(tabref.canon(acc, we, wf + 1), ref)
 
 
 # ----------------------------------------------------------------------------- prepared-weights (table) MAC
@@ -204,11 +225,15 @@ def test_mac_tab_exhaustive_pairs(we, wf, rnd):
     X, W = X.ravel(), W.ravel()
     acc_all = canon_words(we, wf + 1)
     accs = np.concatenate([acc_all[:5], acc_all[5::23]])
+    rng = np.random.default_rng(9)
+    post = lambda v: tabref.canon(v, we, wf + 1)  # noqa: E731  (the chain canonicalises once)
     for s in range(0, accs.size, 8):
         a = accs[s:s + 8]
         A = np.repeat(a, X.size)
         XX, WW = np.tile(X, a.size), np.tile(W, a.size)
-        _check(c, m, tabref.circuit_inputs(A, XX, WW, we, wf, rnd), oracle.mac(A, XX, WW, we, wf, wf + 1, rnd))
+        exp = oracle.mac(A, XX, WW, we, wf, wf + 1, rnd)
+        # the relaxed accumulator input (arbitrary exp/frac when not normal) gives the same result
+        _check(c, m, tabref.circuit_inputs(tabref.relax(A, we, wf + 1, rng), XX, WW, we, wf, rnd), exp, post)
 
 
 @pytest.mark.parametrize("we,wf", [(5, 7), (4, 6), (6, 5)])
@@ -224,7 +249,8 @@ def test_mac_tab_random(we, wf, rnd):
     half = N // 2
     p = oracle.mul(x[:half], w[:half], we, wf, wf + 1, rnd)
     acc[:half] = np.where(rng.random(half) < 0.5, p ^ np.uint32(1 << (wf + 1 + we)), acc[:half])
-    _check(c, m, tabref.circuit_inputs(acc, x, w, we, wf, rnd), oracle.mac(acc, x, w, we, wf, wf + 1, rnd))
+    _check(c, m, tabref.circuit_inputs(tabref.relax(acc, we, wf + 1, rng), x, w, we, wf, rnd),
+           oracle.mac(acc, x, w, we, wf, wf + 1, rnd), lambda v: tabref.canon(v, we, wf + 1))
 
 
 # ----------------------------------------------------------------------------- extended class
@@ -257,4 +283,5 @@ def test_extended_mac_and_mac_tab_random(we, wf, rnd):
     c = fpgen.build_mac(we, wf, wfo, rnd)
     _check(c, lutmap.map_aig(c.g, c.outputs), [acc, x, w], exp)
     ct = fpgen.build_mac_tab(we, wf, rnd, wfo)
-    _check(ct, lutmap.map_aig(ct.g, ct.outputs), tabref.circuit_inputs(acc, x, w, we, wf, rnd, wfo), exp)
+    _check(ct, lutmap.map_aig(ct.g, ct.outputs), tabref.circuit_inputs(tabref.relax(acc, we, wfo, rng), x, w, we, wf, rnd, wfo),
+           exp, lambda v: tabref.canon(v, we, wfo))
