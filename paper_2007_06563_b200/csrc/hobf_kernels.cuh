@@ -166,10 +166,10 @@ struct TabTap {
   }
 };
 
-// KW3: kernel width fixed at 3 (inner loop unrolled).  PF: software pipeline --
-// the record of tap t+2 and the table entry of tap t+1 are loaded while the
-// MAC of tap t runs (for the latency-bound small-batch configs).
-template <class F, int NT, int MINB, bool KW3, bool PF>
+// KW3: kernel width fixed at 3 (inner loop unrolled).  PD > 0: software
+// pipeline -- the table entries of taps t+1..t+PD and the record of tap t+PD+1
+// are in flight while the MAC of tap t runs (latency-bound configs, large tables).
+template <class F, int NT, int MINB, bool KW3, int PD>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   const int G = (a.cout + 31) >> 5;
   const int g = blockIdx.y;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   auto rec_at = [&](int c, int kh, int kw) { return __ldg(rbase + c * cstride + kh * Wp + kw); };
   auto tblock = [&](int c, int kh, int kw) { return tbase + ((int64_t)(kh * KW + kw) * a.cin + c) * tstride; };
 
-  if (!PF) {
+  if constexpr (PD == 0) {
 #pragma unroll 1
     for (int c = 0; c < a.cin; c++) {
 #pragma unroll 1
@@ -208,19 +208,24 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
       }
     }
   } else {
-    TapIter tr, tt;  // tap of the next record / of the next table entry
-    uint32_t rn = rec_at(0, 0, 0);
-    TabTap<F> nxt;
-    nxt.load(rn, tblock(0, 0, 0), a);
-    tt.next(a.kh, KW);
-    tr = tt;
-    rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
-    tr.next(a.kh, KW);
+    // ring of PD taps whose operands are loaded; the record of tap t+PD is one further ahead
     const int taps = a.cin * a.kh * KW;
+    TabTap<F> q[PD > 0 ? PD : 1];
+    TapIter tt, tr;  // tap of the next table entry to load / of the next record to load
+#pragma unroll
+    for (int i = 0; i < PD; i++) {
+      if (tt.c < a.cin) q[i].load(rec_at(tt.c, tt.kh, tt.kw), tblock(tt.c, tt.kh, tt.kw), a);
+      tt.next(a.kh, KW);
+    }
+    tr = tt;
+    uint32_t rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+    tr.next(a.kh, KW);
 #pragma unroll 1
     for (int t = 0; t < taps; t++) {
-      TabTap<F> cur = nxt;
-      if (tt.c < a.cin) nxt.load(rn, tblock(tt.c, tt.kh, tt.kw), a);
+      TabTap<F> cur = q[0];
+#pragma unroll
+      for (int i = 0; i + 1 < PD; i++) q[i] = q[i + 1];
+      if (tt.c < a.cin) q[PD - 1].load(rn, tblock(tt.c, tt.kh, tt.kw), a);
       tt.next(a.kh, KW);
       rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
       tr.next(a.kh, KW);
@@ -274,19 +279,23 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   auto grid = [&](int threads) { return dim3((unsigned)((npix + threads - 1) / threads), gy); };
   const bool k3 = a.kw == 3;
   int variant = a.variant;
+  const int64_t warps = (npix + 31) / 32 * gy;
   if (variant == 0) {
-    // auto: the software-pipelined kernel when the table rows do not stay L1
-    // resident (wF >= 8) or when there are fewer than ~4 warps per SMSP to hide
-    // load latency; otherwise the KW=3-unrolled kernel at <= 56 registers.
-    const int64_t warps = (npix + 31) / 32 * gy;
-    variant = (F::WF >= 8 || warps < 148 * 4 * 4) ? 4 : 3;
+    // auto: with fewer warps than SMSPs the reduction chains are latency-bound:
+    // one-warp CTAs (so every SM gets work) running the software-pipelined
+    // kernel; the pipelined kernel also when the table rows do not stay L1
+    // resident (wF >= 8) or there are < ~4 warps per SMSP to hide load latency;
+    // otherwise the KW=3-unrolled kernel at <= 56 registers.
+    variant = warps < 148 * 4 * 2 ? 5 : ((F::WF >= 8 || warps < 148 * 4 * 4) ? 4 : 3);
   }
-  if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
-    conv_tab_kernel<F, 128, 1, false, true><<<grid(128), 128, 0, s>>>(a);
+  if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
+    conv_tab_kernel<F, 32, 1, false, 3><<<grid(32), 32, 0, s>>>(a);
+  } else if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
+    conv_tab_kernel<F, 128, 1, false, 1><<<grid(128), 128, 0, s>>>(a);
   } else if (k3) {     // kernel width 3 unrolled, <= 56 registers (9 CTAs / SM)
-    conv_tab_kernel<F, 128, 9, true, false><<<grid(128), 128, 0, s>>>(a);
+    conv_tab_kernel<F, 128, 9, true, 0><<<grid(128), 128, 0, s>>>(a);
   } else {
-    conv_tab_kernel<F, 128, 9, false, false><<<grid(128), 128, 0, s>>>(a);
+    conv_tab_kernel<F, 128, 9, false, 0><<<grid(128), 128, 0, s>>>(a);
   }
   return cudaGetLastError();
 }
