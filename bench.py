@@ -51,6 +51,9 @@ def parse_args(argv=None):
                     help="conv kernel: gates = full lop3 MAC (hobf_conv2d); tables = prepared weights "
                          "(hobf_prepare_weights + hobf_conv2d_prepared); auto = tables when the format has them")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="time every format of the config (C5 format sweep)")
+    ap.add_argument("--weights-per-step", action="store_true",
+                    help="re-quantise and re-prepare the weights inside every timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-macs", type=float, default=1.2e9,
                     help="MACs of the bounded oracle sample (about 10 s on 16 host cores)")
@@ -262,10 +265,8 @@ def run_gpu(a, dist):
         else:
             H.quantize_pack(we, wf, x.view(rows_x, cfg.cin), rnd, out=xp, stream=st)
             launches[0] += H.last_launch_count()
-        H.quantize_pack(we, wf, wt, rnd, out=wp, stream=st); launches[0] += H.last_launch_count()
-        if use_tab:
-            H.prepare_weights(f, wp, cfg.kh, cfg.kw, cfg.cin, cfg.cout, out=wtab, stream=st)
-            launches[0] += H.last_launch_count()
+        if a.weights_per_step:
+            prep_weights(st)
         if conv_ev:
             conv_ev[0].record(st)
         if use_tab:
@@ -279,6 +280,23 @@ def run_gpu(a, dist):
             conv_ev[1].record(st)
         H.unpack_f32(we, f.wfo, yp, rows_y, cfg.cout, out=y, stream=st); launches[0] += H.last_launch_count()
 
+    def prep_weights(st):
+        # the layer's weights: quantise + bitslice (a1) and the per-weight product tables;
+        # done once per layer (kernel data pre-transformed) unless --weights-per-step
+        H.quantize_pack(we, wf, wt, rnd, out=wp, stream=st); launches[0] += H.last_launch_count()
+        if use_tab:
+            H.prepare_weights(f, wp, cfg.kh, cfg.kw, cfg.cin, cfg.cout, out=wtab, stream=st)
+            launches[0] += H.last_launch_count()
+
+    prep_weights(stream)
+    torch.cuda.synchronize()
+    pw0, pw1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.fill_(1)
+    pw0.record(stream)
+    prep_weights(stream)
+    pw1.record(stream)
+    torch.cuda.synchronize()
+    weight_prep_ms = pw0.elapsed_time(pw1)
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
@@ -382,8 +400,12 @@ def run_gpu(a, dist):
         "config": {"workload": f"{cfg.name}: {cfg.text}", "format": f"e{we}m{wf}", "round": a.round,
                    "mac_class": "extended" if a.extended else "single", "relu": a.relu, "global_batch": n * dist.world, "per_gpu_batch": n,
                    "dense_macs_per_step": macs_rank * dist.world, "l2": "flushed (256 MiB write) between timed steps",
-                   "step": ("quantize_activations(x) + quantize_pack(w) + prepare_weights + conv2d_prepared + unpack_f32(y)"
-                            if use_tab else "quantize_pack(x) + quantize_pack(w) + conv2d + unpack_f32(y)"),
+                   "step": (("quantize_activations(x) + conv2d_prepared + unpack_f32(y)" if use_tab else
+                              "quantize_pack(x) + conv2d + unpack_f32(y)") +
+                             (" + weight prep" if a.weights_per_step else
+                              "; weights prepared once per layer (quantize_pack(w) + prepare_weights, P:203), "
+                              "timed separately as weight_prep_ms")),
+                   "weight_prep_ms": weight_prep_ms,
                    "parallelism": f"dp{dist.world} (batch shards, no collective)"},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlop3/s",
                      "frac": achieved / peak, "traffic": None,
@@ -406,6 +428,93 @@ def run_gpu(a, dist):
     return 0
 
 
+def run_sweep(a, dist):
+    """--config C5 --sweep: every format of the sweep (configs[4]), each timed on the
+    device like the main line (quantize + prepare + conv + unpack per step); prints one
+    JSON line whose value is all formats' dense MACs / their summed step time, with the
+    per-format MAC/s and roofline fractions under "per_format"."""
+    import torch
+    from paper_2007_06563_b200 import hobf as H
+
+    torch.cuda.set_device(dist.local)
+    dev = torch.device("cuda", dist.local)
+    cfg = inputs.CONFIGS[a.config]
+    rnd = 0 if a.round == "rne" else 1
+    x_np, w_np = inputs.draw(cfg, shard=dist.rank)
+    x = torch.from_numpy(x_np).to(dev)
+    wt = torch.from_numpy(w_np.reshape(-1, cfg.cout)).to(dev)
+    rows_y = cfg.n * cfg.ho * cfg.wo
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    per, tot_ms, tot_macs, launches = {}, 0.0, 0, 0
+    peak = N_SM * LOP3_PER_SM_CLK * SM_MAX_MHZ_FALLBACK * 1e6
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    for (we, wf) in cfg.formats:
+        f = H.Fmt(we, wf, rnd, extended=a.extended)
+        wp = H.quantize_pack(we, wf, wt, rnd)
+        wtab = H.prepare_weights(f, wp, cfg.kh, cfg.kw, cfg.cin, cfg.cout)
+        xrec = H.quantize_activations(f, x, cfg.pad)
+        yp = torch.empty(H.planes_shape(rows_y, cfg.cout, f.nout), dtype=torch.int32, device=dev)
+        y = torch.empty((rows_y, cfg.cout), dtype=torch.float32, device=dev)
+
+        def step(cev=None):
+            n_l = 0
+            H.quantize_activations(f, x, cfg.pad, out=xrec); n_l += H.last_launch_count()
+            if a.weights_per_step:
+                H.quantize_pack(we, wf, wt, rnd, out=wp); n_l += H.last_launch_count()
+                H.prepare_weights(f, wp, cfg.kh, cfg.kw, cfg.cin, cfg.cout, out=wtab); n_l += H.last_launch_count()
+            if cev:
+                cev[0].record(stream)
+            H.conv2d_prepared(f, xrec, cfg.n, cfg.h, cfg.w, cfg.cin, wtab, cfg.kh, cfg.kw, cfg.cout, cfg.stride,
+                              cfg.pad, a.relu, out=yp); n_l += H.last_launch_count()
+            if cev:
+                cev[1].record(stream)
+            H.unpack_f32(we, f.wfo, yp, rows_y, cfg.cout, out=y); n_l += H.last_launch_count()
+            return n_l
+
+        for _ in range(a.warmup):
+            step()
+        K = a.steps
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(K):
+            flush.fill_(k)
+            ev[k][0].record(stream)
+            launches += step(cev[k])
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        ms = dist.max(sum(s_.elapsed_time(e_) for s_, e_ in ev))
+        cms = dist.max(sum(s_.elapsed_time(e_) for s_, e_ in cev))
+        G = H.gate_count(f)["mac_tab"]
+        macs = cfg.macs() * K * dist.world
+        per[f"e{we}m{wf}"] = {"mac_per_s": macs / (ms / 1e3), "conv_mac_per_s": macs / (cms / 1e3), "G": G,
+                             "roofline_frac": cfg.macs() * K * G / 32 / (cms / 1e3) / peak}
+        tot_ms += ms
+        tot_macs += macs
+        del wtab, xrec, yp, y, wp
+    clk = clocks.stop()
+    if dist.rank == 0:
+        worst = min(v["roofline_frac"] for v in per.values())
+        best = max(v["roofline_frac"] for v in per.values())
+        print(json.dumps({
+            "metric": METRIC, "value": tot_macs / (tot_ms / 1e3), "unit": "MAC/s", "n_gpus": dist.world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": tot_ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "sweep e{4,5,6}m{2..10} custom FP, bitsliced u32 lop3",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.text}", "round": a.round, "formats": len(cfg.formats),
+                       "per_gpu_batch": cfg.n, "l2": "flushed (256 MiB write) between timed steps",
+                       "step": "for every format: quantize_activations + conv2d_prepared + unpack_f32 (weights "
+                               "prepared once per layer" + (", and again every step)" if a.weights_per_step else ")"),
+                       "parallelism": f"dp{dist.world} (batch shards, no collective)"},
+            "roofline": {"bound": "alu", "unit": "fraction of LOP3 roof per format",
+                         "frac_min": worst, "frac_max": best, "peak_tlop3_s": peak / 1e12},
+            "per_format": per, "gpu_launches": launches, "clocks": clk}), flush=True)
+    return 0
+
+
 def main(argv=None):
     a = parse_args(argv)
     dist = Dist()
@@ -415,6 +524,8 @@ def main(argv=None):
     import torch
     dist.init("nccl" if torch.cuda.is_available() else "gloo")
     try:
+        if a.sweep:
+            return run_sweep(a, dist)
         return run_gpu(a, dist)
     finally:
         dist.done()

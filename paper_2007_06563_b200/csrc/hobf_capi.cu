@@ -310,21 +310,37 @@ __global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restr
   const int npi = (3 + we + wf + 3) / 4 * 4;
   const int rows = tab_rows(wf);
   const int npt = (tab_width(we, wfo) + 3) / 4 * 4;
-  const int64_t items = wrows * G * rows;
+  // item = (weight row, group, chunk of 32 table rows): the weight is decoded once
+  // per item and reused for the chunk's rows.
+  const int chunks = (rows + 31) / 32;
+  const int64_t items = wrows * G * chunks;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
-    const int r = (int)(it % rows);
-    const int64_t grp = it / rows;  // (weight row, group)
+    const int r0 = (int)(it % chunks) * 32;
+    const int64_t grp = it / chunks;  // (weight row, group)
     const uint32_t mine = lane < npi ? __ldg(wplanes + grp * npi + lane) : 0u;
     uint32_t w = 0u;
     for (int j = 0; j < 3 + we + wf; j++) w |= ((__shfl_sync(0xffffffffu, mine, j) >> lane) & 1u) << j;
-    const uint32_t e = tab_entry(w, r, we, wf, wfo, rnd);
-    uint32_t out = 0u;
-    for (int j = 0; j < npt; j++) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (e >> j) & 1u);
-      if (lane == j) out = bal;
+    const int r1 = min(rows, r0 + 32);
+    constexpr int U = 4;  // rows in flight (independent entry computations and ballots)
+    for (int r = r0; r < r1; r += U) {
+      uint32_t e[U], out[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        e[u] = r + u < r1 ? tab_entry(w, r + u, we, wf, wfo, rnd) : 0u;
+        out[u] = 0u;
+      }
+      for (int j = 0; j < npt; j++) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const uint32_t bal = __ballot_sync(0xffffffffu, (e[u] >> j) & 1u);
+          out[u] = lane == j ? bal : out[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (lane < npt && r + u < r1) wtab[(grp * rows + r + u) * npt + lane] = out[u];
     }
-    if (lane < npt) wtab[it * npt + lane] = out;
   }
 }
 
@@ -525,7 +541,7 @@ hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t
   if (!d_w_planes || !d_wtab || !aligned16(d_w_planes) || !aligned16(d_wtab)) return HOBF_EINVAL;
   const int G = (cout + 31) / 32;
   const int64_t wrows = (int64_t)kh * kw * cin;
-  const int64_t items = wrows * G * tab_rows(f.wf);
+  const int64_t items = wrows * G * ((tab_rows(f.wf) + 31) / 32);
   build_wtab_kernel<<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(d_w_planes, wrows, G, f.we, f.wf,
                                                                           hobf_out_wf(f), f.round, d_wtab);
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;

@@ -194,7 +194,31 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   auto rec_at = [&](int c, int kh, int kw) { return __ldg(rbase + c * cstride + kh * Wp + kw); };
   auto tblock = [&](int c, int kh, int kw) { return tbase + ((int64_t)(kh * KW + kw) * a.cin + c) * tstride; };
 
-  if constexpr (PD == 0) {
+  if constexpr (PD == 0 && KW3) {
+    // the 3 records of the next kernel row are loaded while this row's 3 MACs run
+    uint32_t rn[3];
+#pragma unroll
+    for (int kw = 0; kw < 3; kw++) rn[kw] = rec_at(0, 0, kw);
+    int nc = 0, nkh = 0;
+#pragma unroll 1
+    for (int row = 0; row < a.cin * a.kh; row++) {
+      const int c = nc, kh = nkh;
+      uint32_t rc[3];
+#pragma unroll
+      for (int kw = 0; kw < 3; kw++) rc[kw] = rn[kw];
+      if (++nkh == a.kh) { nkh = 0; ++nc; }
+      if (nc < a.cin) {
+#pragma unroll
+        for (int kw = 0; kw < 3; kw++) rn[kw] = rec_at(nc, nkh, kw);
+      }
+#pragma unroll
+      for (int kw = 0; kw < 3; kw++) {
+        TabTap<F> tp;
+        tp.load(rc[kw], tblock(c, kh, kw), a);
+        F::mac_tab(acc, tp.T, tp.EA, tp.SX);
+      }
+    }
+  } else if constexpr (PD == 0) {
 #pragma unroll 1
     for (int c = 0; c < a.cin; c++) {
 #pragma unroll 1
