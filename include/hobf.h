@@ -154,6 +154,21 @@ hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, 
                                  int32_t stride, int32_t pad, int32_t relu, uint32_t* d_y_planes,
                                  hobf_stream stream);
 
+/* hobf_conv2d_prepared with an explicit kernel schedule (tests, benchmarks):
+ * variant 0 = automatic (what hobf_conv2d_prepared uses; the environment
+ * variable HOBF_CONV_VARIANT overrides it there), 3 = one thread per (pixel,
+ * 32-Cout group), kernel row of 3 taps unrolled, <= 56 registers; 4 = table
+ * entry of the next tap prefetched (large tables); 5 = one-warp CTAs with a
+ * 3-deep prefetch ring (fewer warps than SMSPs); 6 = three kernel rows (one
+ * input channel) per unrolled loop body, <= 64 registers.  Variants 3 and 6
+ * need kw == 3 (others fall back to the generic loop).  Every variant runs the
+ * same circuit over the same serial (c, kh, kw) order: results are identical.
+ * Unknown variants -> HOBF_EINVAL. */
+hobf_status hobf_conv2d_prepared_variant(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
+                                         int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw,
+                                         int32_t cout, int32_t stride, int32_t pad, int32_t relu,
+                                         uint32_t* d_y_planes, int32_t variant, hobf_stream stream);
+
 /* LOP3 issue-rate microbenchmark (roofline denominator): launches `blocks` x
  * `threads` threads, each issuing `iters` x 128 dependent-free lop3 ops;
  * *lop3_per_launch receives the thread-op count.  d_sink: >= 4 KiB device. */

@@ -594,8 +594,17 @@ hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, i
 hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w, int32_t cin,
                                  const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
                                  int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
+  return hobf_conv2d_prepared_variant(f, d_xrec, n, h, w, cin, d_wtab, kh, kw, cout, stride, pad, relu, d_y_planes,
+                                      conv_tab_variant(), stream);
+}
+
+hobf_status hobf_conv2d_prepared_variant(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
+                                         int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw,
+                                         int32_t cout, int32_t stride, int32_t pad, int32_t relu,
+                                         uint32_t* d_y_planes, int32_t variant, hobf_stream stream) {
   const uint32_t* d_x_planes = d_xrec;
   g_last_launches = 0;
+  if (variant != 0 && (variant < 3 || variant > 6)) return HOBF_EINVAL;
   if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
     return HOBF_EINVAL;
   if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)
@@ -613,7 +622,7 @@ hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, 
   a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
-  a.variant = conv_tab_variant();
+  a.variant = variant;
   a.row_mul = 1u << 12;
   for (int j = 0; j < 32; j++) a.lift[j] = 1u << (31 - j);
   a.one = 1;

@@ -166,10 +166,11 @@ struct TabTap {
   }
 };
 
-// KW3: kernel width fixed at 3 (inner loop unrolled).  PD > 0: software
-// pipeline -- the table entries of taps t+1..t+PD and the record of tap t+PD+1
-// are in flight while the MAC of tap t runs (latency-bound configs, large tables).
-template <class F, int NT, int MINB, bool KW3, int PD>
+// KW3: kernel width fixed at 3 (inner loop unrolled); RU kernel rows per
+// unrolled loop body.  PD > 0: software pipeline -- the table entries of taps
+// t+1..t+PD and the record of tap t+PD+1 are in flight while the MAC of tap t
+// runs (latency-bound configs, large tables).
+template <class F, int NT, int MINB, bool KW3, int PD, int RU = 1>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   const int G = (a.cout + 31) >> 5;
   const int g = blockIdx.y;
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
 #pragma unroll
     for (int kw = 0; kw < 3; kw++) rn[kw] = rec_at(0, 0, kw);
     int nc = 0, nkh = 0;
-#pragma unroll 1
+#pragma unroll RU
     for (int row = 0; row < a.cin * a.kh; row++) {
       const int c = nc, kh = nkh;
       uint32_t rc[3];
@@ -309,10 +310,13 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     // one-warp CTAs (so every SM gets work) running the software-pipelined
     // kernel; the pipelined kernel also when the table rows do not stay L1
     // resident (wF >= 8) or there are < ~4 warps per SMSP to hide load latency;
-    // otherwise the KW=3-unrolled kernel at <= 56 registers.
-    variant = warps < 148 * 4 * 2 ? 5 : ((F::WF >= 8 || warps < 148 * 4 * 4) ? 4 : 3);
+    // otherwise the KW=3 kernel with three kernel rows per unrolled loop body
+    // (more independent work in view of the scheduler) at <= 64 registers.
+    variant = warps < 148 * 4 * 2 ? 5 : (F::WF >= 8 ? 4 : (k3 ? 6 : 3));
   }
-  if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
+  if (variant == 6 && k3) {  // KW=3, 3 kernel rows (one input channel) per unrolled body, <= 64 registers
+    conv_tab_kernel<F, 128, 8, true, 0, 3><<<grid(128), 128, 0, s>>>(a);
+  } else if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
     conv_tab_kernel<F, 32, 1, false, 3><<<grid(32), 32, 0, s>>>(a);
   } else if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
     conv_tab_kernel<F, 128, 1, false, 1><<<grid(128), 128, 0, s>>>(a);

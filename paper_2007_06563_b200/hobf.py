@@ -91,6 +91,9 @@ _lib.hobf_prepare_weights.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, 
 _lib.hobf_conv2d_prepared.restype = _i32
 _lib.hobf_conv2d_prepared.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _i32,
                                       _p, _p]
+_lib.hobf_conv2d_prepared_variant.restype = _i32
+_lib.hobf_conv2d_prepared_variant.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32,
+                                              _i32, _p, _i32, _p]
 _lib.hobf_xrec_words.restype = _i64
 _lib.hobf_xrec_words.argtypes = [_i32, _i32, _i32, _i32, _i32]
 _lib.hobf_prepare_activations.restype = _i32
@@ -107,7 +110,7 @@ _lib.hobf_version.restype = ctypes.c_char_p
 SYMBOLS = ["hobf_nbits", "hobf_out_wf", "hobf_nplanes", "hobf_planes_words", "hobf_pack", "hobf_quantize_pack",
            "hobf_unpack", "hobf_unpack_f32", "hobf_conv2d", "hobf_mac_planes", "hobf_gate_count",
            "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version",
-           "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_xrec_words",
+           "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_conv2d_prepared_variant", "hobf_xrec_words",
            "hobf_prepare_activations", "hobf_quantize_activations"]
 
 
@@ -266,12 +269,20 @@ def quantize_activations(f: Fmt, x: torch.Tensor, pad: int, out=None, stream=Non
 
 def conv2d_prepared(f: Fmt, xrec: torch.Tensor, n: int, h: int, w: int, cin: int, wtab: torch.Tensor,
                     kh: int, kw: int, cout: int, stride: int = 1, pad: int = 1, relu: int = 0, out=None,
-                    stream=None) -> torch.Tensor:
-    """Conv on prepared activations (same pad) and prepared weights -> output planes."""
+                    stream=None, variant: int | None = None) -> torch.Tensor:
+    """Conv on prepared activations (same pad) and prepared weights -> output planes.
+    variant: None = hobf_conv2d_prepared (automatic schedule), else
+    hobf_conv2d_prepared_variant with that kernel schedule (identical results)."""
     ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
     out = _new_planes(max(n * ho * wo, 0), cout, f.nout, xrec.device, out)
-    _check("hobf_conv2d_prepared", _lib.hobf_conv2d_prepared(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw,
-                                                             cout, stride, pad, int(relu), _ptr(out), _stream(stream)))
+    if variant is None:
+        _check("hobf_conv2d_prepared", _lib.hobf_conv2d_prepared(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw,
+                                                                 cout, stride, pad, int(relu), _ptr(out),
+                                                                 _stream(stream)))
+    else:
+        _check("hobf_conv2d_prepared_variant",
+               _lib.hobf_conv2d_prepared_variant(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw, cout, stride,
+                                                 pad, int(relu), _ptr(out), int(variant), _stream(stream)))
     return out
 
 

@@ -246,6 +246,31 @@ def test_conv_prepared_full_vs_oracle(we, wf):
             assert np.array_equal(got, gpu_conv(x, w, f, relu=relu, prepared=False))
 
 
+@pytest.mark.parametrize("variant", [3, 4, 5, 6])
+@pytest.mark.parametrize("we,wf,kh,kw", [(5, 3, 3, 3), (4, 6, 2, 3), (5, 10, 3, 3), (6, 2, 3, 2)])
+def test_conv_prepared_every_schedule(variant, we, wf, kh, kw):
+    """Every kernel schedule of hobf_conv2d_prepared_variant gives the oracle's words:
+    several 128-pixel CTAs with a ragged tail, a ragged last Cout group, cin not a
+    multiple of the 3-row unroll (kh = 2), stride 2, specials present."""
+    H = hobf()
+    n, h, w, cin, cout, stride, pad = 3, 11, 13, 5, 40, 1, 1
+    x, wt = inputs.small_case(91 + variant, n, h, w, cin, cout, "normal", 0.4, kh=kh, kw=kw)
+    x[0, 0, :3, 0] = [np.inf, np.nan, -0.0]
+    wt[0, 0, 1, :2] = [np.inf, 0.0]
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd)
+        for s_ in (stride, 2):
+            exp = oracle_conv(x, wt, f, stride=s_, pad=pad, relu=0)
+            xp = H.quantize_pack(we, wf, torch.from_numpy(x.reshape(-1, cin)).cuda(), rnd)
+            wp = H.quantize_pack(we, wf, torch.from_numpy(wt.reshape(-1, cout)).cuda(), rnd)
+            tab = H.prepare_weights(f, wp, kh, kw, cin, cout)
+            xr = H.prepare_activations(f, xp, n, h, w, cin, pad)
+            yp = H.conv2d_prepared(f, xr, n, h, w, cin, tab, kh, kw, cout, s_, pad, 0, variant=variant)
+            ho, wo = H.conv_out_hw(h, w, kh, kw, s_, pad)
+            got = to_np_words(H.unpack(we, f.wfo, yp, n * ho * wo, cout)).reshape(exp.shape)
+            assert np.array_equal(got, exp), (variant, rnd, s_, np.argwhere(got != exp)[:5])
+
+
 @pytest.mark.parametrize("shape", [
     # n, h, w, cin, cout, kh, kw, stride, pad
     (2, 9, 7, 40, 50, 3, 3, 1, 1),     # ragged cin and cout, several tiles
