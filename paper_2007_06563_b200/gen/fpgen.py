@@ -161,14 +161,21 @@ def lzc(g: AIG, v):
     return cnt, z
 
 
-def normalize_left(g: AIG, v):
+def normalize_left(g: AIG, v, max_shift=None):
     """Leading-zero normalisation by successive detection: for 2^j from the
     largest power of two down, if the top 2^j bits of the current vector are
     all zero, shift it left by 2^j.  Returns (normalised v, shift count bits
-    LSB first, all_zero).  Same result as lzc + shift_left, fewer gates."""
+    LSB first, all_zero).  Same result as lzc + shift_left, fewer gates.
+
+    ``max_shift``: a bound on the shift any nonzero input needs (its leading
+    one is never below bit L-1-max_shift); only bitlen(max_shift) stages are
+    built.  all_zero stays exact: a nonzero input always ends with its leading
+    one at the top."""
     L = len(v)
     K = 0
-    while (1 << K) < L:
+    if max_shift is None:
+        max_shift = L - 1
+    while (1 << K) <= max_shift:
         K += 1
     cur = list(v)
     cnt = [FALSE] * K
@@ -336,7 +343,12 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
     Z[W + 1] = g.AND(Z[W + 1], g.NOT(sub))
     # normalise: leading-zero count over Z[W+1..0] and left shift
     if norm == "detect":
-        Zn, cnt, zsum = normalize_left(g, Z)
+        # Bound on the left shift: with d >= 2 the difference keeps its leading
+        # one at bit W or W-1 (X >= 1, Y < 1/2 before alignment); with d <= 1
+        # the aligned Y has no bits below position 2 (its LSB lands on the G
+        # position at most), so the exact sum is a multiple of 2^2 and a
+        # nonzero Z has its leading one at bit >= 2: shift <= W - 1 = p + 1.
+        Zn, cnt, zsum = normalize_left(g, Z, max_shift=W - 1)
     else:
         cnt, zsum = lzc(g, Z)
         Zn = shift_left(g, Z, cnt)
