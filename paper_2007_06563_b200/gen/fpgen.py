@@ -113,15 +113,25 @@ def multiply(g: AIG, a, b):
     return ripple_add(g, r0, r1, FALSE, width=W)
 
 
-def shift_right_sticky(g: AIG, v, d, order="small_first", kill=FALSE):
+def shift_right_sticky(g: AIG, v, d, order="small_first", kill=FALSE, clamp=False):
     """Logical right shift of v (LSB first) by the unsigned amount d (bits LSB
     first); returns (shifted, sticky) where sticky = OR of all bits shifted out.
-    If ``kill`` is true the result and the sticky are forced to zero."""
+    If ``kill`` is true the result and the sticky are forced to zero.
+
+    clamp=True: a shift of 2^K - 1 >= len(v) already moves every bit into the
+    sticky, so amounts >= 2^K (and ``kill``) are clamped to 2^K - 1 by OR-ing
+    the high / kill bits into the K low shift bits, and ``kill`` then only has
+    to clear the sticky -- instead of clearing every shifted bit."""
     W = len(v)
     K = 0
     while (1 << K) <= W:
         K += 1
     K = min(K, len(d))
+    if clamp:
+        hi = g.OR(g.OR_many(d[K:]), kill)
+        dd = [g.OR(d[j], hi) for j in range(K)]
+        cur, sticky = shift_right_sticky(g, v, dd, order=order)
+        return cur, g.AND(sticky, g.NOT(kill))
     big = g.OR(g.OR_many(d[K:]), kill)
     cur = list(v)
     sticky = FALSE
@@ -287,7 +297,7 @@ def fp_add(g: AIG, A: FP, B: FP, rnd: int, shift_order="small_first"):
 
 
 def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_first", norm="detect",
-               expo="one_adder", canon_out=True):
+               expo="one_adder", canon_out=True, clamp=True):
     """HOBFLOPS adder F(wE,w) + F(wE,w) -> F(wE,w) (single-path, P:190-198;
     SURVEY 8(c) add; ledger L5-L7).  A must be canonical; B may be
     non-canonical (its exp/frac are ignored when it is zero or special).
@@ -320,21 +330,24 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
     eY = [g.MUX(swap, a, b) for a, b in zip(A.exp, B.exp)]
     fX = [g.MUX(swap, b, a) for a, b in zip(A.frac, B.frac)]
     fY = [g.MUX(swap, a, b) for a, b in zip(A.frac, B.frac)]
-    hX = g.MUX(swap, hB, hA)
+    # X (the larger magnitude) is normal unless both operands are zero (zeros
+    # sort below every normal; specials are overridden below), so its hidden
+    # bit is wired to 1 and the both-zero case is flagged explicitly.
+    hX = TRUE
     hY = g.MUX(swap, hA, hB)
     sX = g.MUX(swap, B.sign, A.sign)
     sub = g.XOR(A.sign, B.sign)
     kill = FALSE if B.canonical else g.AND(g.NOT(swap), B.zero)
     if not A.canonical:
         kill = g.OR(kill, g.AND(swap, A.zero))
-    both_zero = FALSE if A.canonical else g.AND(A.zero, B.zero)
+    both_zero = g.AND(A.zero, B.zero)
 
     # d = eX - eY >= 0
     d = ripple_add(g, eX, [g.NOT(x) for x in eY], TRUE, width=we)
     # alignment: W = p + 2 positions (significand + G + R), then sticky
     W = p + 2
     mY = [FALSE, FALSE] + list(fY) + [hY]
-    yv, ys = shift_right_sticky(g, mY, d, order=shift_order, kill=kill)
+    yv, ys = shift_right_sticky(g, mY, d, order=shift_order, kill=kill, clamp=clamp)
     mX = [FALSE, FALSE] + list(fX) + [hX]
     # adder over W+1 bits: position 0 = sticky, 1..W = shifted significand
     xo = [FALSE] + mX
@@ -375,7 +388,7 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
     ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])
 
     nan = g.OR_many([A.nan, B.nan, g.AND(g.AND(A.inf, B.inf), sub)])
-    zsum = g.OR(zsum, both_zero)   # with a non-canonical A the datapath is garbage when both are zero
+    zsum = g.OR(zsum, both_zero)   # both zero: the datapath (hidden bit of X = 1) is not zero
     fin_nz = g.AND(g.NOT(special), g.NOT(zsum))
     normal = g.AND(fin_nz, g.AND(g.NOT(ovf), g.NOT(unf)))
     exc1 = g.OR(special, g.AND(fin_nz, ovf))
