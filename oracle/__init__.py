@@ -59,6 +59,7 @@ def lib():
         L.ref_relu_batch.argtypes = [P, P, i64, i32, i32]
         L.ref_canon_batch.argtypes = [P, P, i64, i32, i32]
         L.ref_encode_f32_batch.argtypes = [P, P, i64, i32, i32, i32]
+        L.ref_convert_batch.argtypes = [P, P, i64, i32, i32, i32, i32]
         L.ref_decode_f64_batch.argtypes = [P, P, i64, i32, i32]
         L.ref_mac_batch.argtypes = [P, P, P, i64, i32, i32, i32, i32]
         L.ref_conv2d.restype = i32
@@ -118,6 +119,30 @@ def canon(a, we, wf) -> np.ndarray:
     out = np.empty(a.shape, np.uint32)
     lib().ref_canon_batch(_ptr(a), _ptr(out), a.size, we, wf)
     return out
+
+
+def convert(a, we, wf_in, wf_out, mode=RNE) -> np.ndarray:
+    """Re-round F(we, wf_in) words into F(we, wf_out) (ref_convert: the layer
+    epilogue of a chained network)."""
+    a = _u32(a)
+    out = np.empty_like(a)
+    lib().ref_convert_batch(_ptr(a), _ptr(out), a.size, we, wf_in, wf_out, mode)
+    return out
+
+
+def conv_chain(x, layers, we, mode=RNE, nthreads=None) -> np.ndarray:
+    """A chain of conv layers in the custom format: x = F(we, wf0) NHWC
+    words; layers = [(w_words, wf, stride, pad, relu, extended), ...] where wf is
+    that layer's input fraction width.  Each layer: conv2d at its MAC width,
+    then (except after the last) convert to the next layer's wf.  Returns the
+    last layer's accumulator-format words."""
+    y = x
+    for i, (wts, wf, stride, pad, relu, ext) in enumerate(layers):
+        wf_out = 2 * wf + 1 if ext else wf + 1
+        y = conv2d(y, wts, we, wf, wf_out, mode, stride, pad, relu, nthreads)
+        if i + 1 < len(layers):
+            y = convert(y, we, wf_out, layers[i + 1][1], mode)
+    return y
 
 
 def encode_f32(x, we, wf, mode=RNE) -> np.ndarray:

@@ -189,6 +189,19 @@ uint32_t ref_canon(uint32_t a, int we, int wf) {
     return round_to(x.sign, x.M, x.e, we, wf, RND_RNE);
 }
 
+/* ref_convert (with the extended class "rounding is dealt with at the end
+ * of the layer in the activation function"; layers chained in the
+ * bitsliced format): a word of F(wE, wf_in) re-rounded into
+ * the next layer's F(wE, wf_out) -- round_to of its exact value (one rounding,
+ * RNE or RTZ; widening is exact).  Zero / inf keep their sign, NaN stays NaN.
+ * The exponent width is unchanged, so only rounding up to the next binade can
+ * overflow (-> inf, L5); nothing underflows. */
+uint32_t ref_convert(uint32_t a, int we, int wf_in, int wf_out, int mode) {
+    val_t x = decode(a, we, wf_in);
+    if (x.cls != CLS_NORMAL) return enc_special(x.cls, x.sign, we, wf_out);
+    return round_to(x.sign, x.M, x.e, we, wf_out, mode);
+}
+
 /* from_binary32 (L13): exact rational of the float32 (IEEE
  * subnormals included), then round_to; NaN -> NaN, +-inf -> +-inf, +-0 -> +-0. */
 uint32_t ref_encode_f32(float f, int we, int wf, int mode) {
@@ -235,6 +248,10 @@ void ref_relu_batch(const uint32_t* a, uint32_t* out, int64_t n, int we, int wf)
 
 void ref_canon_batch(const uint32_t* a, uint32_t* out, int64_t n, int we, int wf) {
     for (int64_t i = 0; i < n; i++) out[i] = ref_canon(a[i], we, wf);
+}
+
+void ref_convert_batch(const uint32_t* a, uint32_t* out, int64_t n, int we, int wf_in, int wf_out, int mode) {
+    for (int64_t i = 0; i < n; i++) out[i] = ref_convert(a[i], we, wf_in, wf_out, mode);
 }
 
 void ref_encode_f32_batch(const float* x, uint32_t* out, int64_t n, int we, int wf, int mode) {

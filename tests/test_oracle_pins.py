@@ -383,3 +383,85 @@ def test_conv_metamorphic():
     idx = np.arange(0, y.size, 7)
     assert np.array_equal(oracle.conv2d_sample(x, wt, idx, we, wf, wfo), y.ravel()[idx])
     assert np.array_equal(oracle.conv2d(x, wt, we, wf, wfo, nthreads=1), oracle.conv2d(x, wt, we, wf, wfo, nthreads=5))
+
+
+# ----------------------------------------------------------------------------- layer-epilogue conversion
+
+@pytest.mark.parametrize("we,wf_in,wf_out", [(3, 3, 1), (3, 2, 1), (4, 3, 2), (2, 4, 2), (3, 1, 3)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_convert_exhaustive_vs_rational(we, wf_in, wf_out, mode):
+    """ref_convert (P:262 epilogue rounding) on every canonical word of a tiny
+    format against the exact-rational nearest-grid-point search of pyref."""
+    words = pyref.canonical_words(we, wf_in)
+    got = oracle.convert(np.array(words, dtype=np.uint32), we, wf_in, wf_out, mode)
+    for w, g in zip(words, got):
+        v = pyref.word_to_value(w, we, wf_in)
+        if isinstance(v, str):
+            exp = pyref.value_to_word(v, we, wf_out)
+        else:
+            exp = pyref.value_to_word(pyref.round_value(v, we, wf_out, mode), we, wf_out)
+        assert int(g) == exp, (hex(w), hex(int(g)), hex(exp))
+
+
+def test_convert_matches_ieee_half_and_fp8_casts():
+    """e5m11 -> e5m10 equals numpy's float32 -> float16 RNE cast, and e4m4 -> e4m3
+    equals ml_dtypes' float32 -> float8_e4m3fn cast, wherever both formats are
+    normal (the FloPoCo cores coincide with IEEE there)."""
+    ml = pytest.importorskip("ml_dtypes")
+    rng = np.random.default_rng(5)
+    for we, wfi, wfo, lo, hi, cast in ((5, 11, 10, 2.0 ** -14, 65504.0, np.float16),
+                                       (4, 4, 3, 2.0 ** -6, 448.0, ml.float8_e4m3fn)):
+        top = wfi + we + 1
+        n = 200000
+        words = ((1 << top) | (rng.integers(0, 2, n) << (wfi + we)) | (rng.integers(0, 1 << we, n) << wfi)
+                 | rng.integers(0, 1 << wfi, n)).astype(np.uint32)
+        v = oracle.decode_f64(words, we, wfi)
+        keep = (np.abs(v) >= lo) & (np.abs(v) <= hi)
+        words, v = words[keep], v[keep]
+        lib = np.asarray(v.astype(np.float32).astype(cast).astype(np.float64))
+        ok = np.isfinite(lib) & (np.abs(lib) <= hi)
+        got = oracle.decode_f64(oracle.convert(words, we, wfi, wfo, 0), we, wfo)
+        assert ok.sum() > 1000
+        assert np.array_equal(got[ok], lib[ok])
+
+
+def test_convert_invariants():
+    """Widening is exact (and narrowing it back is the identity); RTZ never
+    increases the magnitude; RNE is within half an ulp; specials keep class and sign."""
+    rng = np.random.default_rng(6)
+    we, wf = 5, 7
+    words = oracle.encode_f32(rng.standard_normal(50000).astype(np.float32) * 8, we, wf)
+    wide = oracle.convert(words, we, wf, 2 * wf + 1)
+    assert np.array_equal(oracle.decode_f64(wide, we, 2 * wf + 1), oracle.decode_f64(words, we, wf))
+    assert np.array_equal(oracle.convert(wide, we, 2 * wf + 1, wf), words)
+    src = oracle.encode_f32(rng.standard_normal(50000).astype(np.float32), we, 10)
+    src = src[oracle.decode_f64(src, we, 10) != 0]
+    v = oracle.decode_f64(src, we, 10)
+    z = oracle.decode_f64(oracle.convert(src, we, 10, 3, 1), we, 3)
+    assert np.all(np.abs(z) <= np.abs(v)) and np.all(np.abs(v - z) < 2.0 ** (np.floor(np.log2(np.abs(v))) - 3))
+    r = oracle.decode_f64(oracle.convert(src, we, 10, 3, 0), we, 3)
+    assert np.all(np.abs(v - r) <= 2.0 ** (np.floor(np.log2(np.abs(v))) - 4))
+    top = 10 + we + 1
+    sp = np.array([0, 1 << (10 + we), 2 << top, (2 << top) | (1 << (10 + we)), 3 << top], dtype=np.uint32)
+    t3 = 3 + we + 1
+    assert list(oracle.convert(sp, we, 10, 3)) == [0, 1 << (3 + we), 2 << t3, (2 << t3) | (1 << (3 + we)), 3 << t3]
+    # rounding up out of the top binade overflows to inf (L5)
+    mx = np.array([(1 << top) | (((1 << we) - 1) << 10) | 1023], dtype=np.uint32)
+    assert oracle.convert(mx, we, 10, 3, 0)[0] == 2 << t3
+    assert oracle.convert(mx, we, 10, 3, 1)[0] == (1 << t3) | (((1 << we) - 1) << 3) | 7
+
+
+def test_conv_chain_is_layerwise():
+    """oracle.conv_chain = conv2d, convert, conv2d (the definition), and a chain
+    whose second layer is a centred identity kernel reproduces the first layer's
+    converted (then widened) output exactly."""
+    from fractions import Fraction
+    we, wf = 5, 3
+    x, w1 = small_conv_case(9, 1, 5, 6, 4, 4, we, wf)
+    ident = np.zeros((3, 3, 4, 4), dtype=np.uint32)
+    one = pyref.value_to_word(Fraction(1), we, wf)
+    for c in range(4):
+        ident[1, 1, c, c] = one
+    y = oracle.conv_chain(x, [(w1, wf, 1, 1, 1, 0), (ident, wf, 1, 1, 0, 0)], we)
+    y1 = oracle.convert(oracle.conv2d(x, w1, we, wf, wf + 1, 0, 1, 1, 1), we, wf + 1, wf)
+    assert np.array_equal(oracle.decode_f64(y, we, wf + 1), oracle.decode_f64(y1, we, wf))
