@@ -154,20 +154,54 @@ hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, 
                                  int32_t stride, int32_t pad, int32_t relu, uint32_t* d_y_planes,
                                  hobf_stream stream);
 
-/* hobf_conv2d_prepared with an explicit kernel schedule (tests, benchmarks):
- * variant 0 = automatic (what hobf_conv2d_prepared uses; the environment
- * variable HOBF_CONV_VARIANT overrides it there), 3 = one thread per (pixel,
- * 32-Cout group), kernel row of 3 taps unrolled, <= 56 registers; 4 = table
- * entry of the next tap prefetched (large tables); 5 = one-warp CTAs with a
- * 3-deep prefetch ring (fewer warps than SMSPs); 6 = three kernel rows (one
- * input channel) per unrolled loop body, <= 64 registers.  Variants 3 and 6
- * need kw == 3 (others fall back to the generic loop).  Every variant runs the
- * same circuit over the same serial (c, kh, kw) order: results are identical.
- * Unknown variants -> HOBF_EINVAL. */
-hobf_status hobf_conv2d_prepared_variant(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
-                                         int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw,
-                                         int32_t cout, int32_t stride, int32_t pad, int32_t relu,
-                                         uint32_t* d_y_planes, int32_t variant, hobf_stream stream);
+/* ---- Conv with an explicit output epilogue / kernel schedule ----------------
+ * Layer chaining ("the OFM stays in the bitsliced format between
+ * layers"; with the extended class "rounding is dealt with at the end
+ * of the layer in the activation function"): after the serial reduction (and
+ * ReLU when relu != 0) every output word of F(we, wfo) is re-rounded into the
+ * NEXT layer's input format F(we, next_wf) (RNE or RTZ as f.round; exact
+ * when next_wf >= wfo; rounding up out of the top binade -> inf; zero / inf
+ * keep their sign) and written in the layout the next layer consumes, so no
+ * unpack / repack runs between layers.
+ *   HOBF_OUT_PLANES        plain output planes F(we, wfo) (= hobf_conv2d[_prepared]);
+ *   HOBF_OUT_NEXT_PLANES   planes of F(we, next_wf): [n*ho*wo][ceil(cout/32)]
+ *                          [roundup(3+we+next_wf, 4)] = the next hobf_conv2d's x;
+ *   HOBF_OUT_NEXT_RECORDS  activation records of F(we, next_wf), zero-padded by
+ *                          next_pad: [n][cout][ho+2*next_pad][wo+2*next_pad]
+ *                          (hobf_xrec_words(n, ho, wo, cout, next_pad) words) =
+ *                          the next hobf_conv2d_prepared's x.  Only the interior
+ *                          is written: the caller's buffer must hold +0 records
+ *                          in the padding border (e.g. zero-filled once; the
+ *                          +0 record of F(we, next_wf) is (2^next_wf) << 20).
+ *                          Needs 3+we+next_wf <= 20 and next_wf <= 10
+ *                          (hobf_conv2d_prepared_ex only).
+ * next_wf / next_pad are ignored for HOBF_OUT_PLANES; inconsistent values ->
+ * HOBF_EINVAL.  The oracle's definition is ref_convert(relu(acc)). */
+typedef enum { HOBF_OUT_PLANES = 0, HOBF_OUT_NEXT_PLANES = 1, HOBF_OUT_NEXT_RECORDS = 2 } hobf_out_mode;
+typedef struct {
+  int32_t mode;     /* hobf_out_mode */
+  int32_t next_wf;  /* next layer's fraction width (same exponent width we) */
+  int32_t next_pad; /* next layer's padding (records only) */
+} hobf_epilogue;
+
+hobf_status hobf_conv2d_ex(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
+                           const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
+                           int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_out, hobf_stream stream);
+
+/* hobf_conv2d_prepared with an epilogue (above) and an explicit kernel
+ * schedule: variant 0 = automatic (what hobf_conv2d_prepared uses; the
+ * environment variable HOBF_CONV_VARIANT overrides it there), 3 = one thread
+ * per (pixel, 32-Cout group), kernel row of 3 taps unrolled, <= 56 registers;
+ * 4 = table entry of the next tap prefetched (large tables); 5 = one-warp CTAs
+ * with a 3-deep prefetch ring (fewer warps than SMSPs); 6 = three kernel rows
+ * (one input channel) per unrolled loop body, <= 64 registers.  Variants 3
+ * and 6 need kw == 3 (others fall back to the generic loop).  Every variant
+ * runs the same circuit over the same serial (c, kh, kw) order: identical
+ * results.  Unknown variants -> HOBF_EINVAL. */
+hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
+                                    int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout,
+                                    int32_t stride, int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_out,
+                                    int32_t variant, hobf_stream stream);
 
 /* LOP3 issue-rate microbenchmark (roofline denominator): launches `blocks` x
  * `threads` threads, each issuing `iters` x 128 dependent-free lop3 ops;

@@ -10,9 +10,11 @@
 
 #include "../../include/hobf.h"
 #include "hobf_internal.h"
+#include "hobf_words.cuh"
 
 using hobf::ConvArgs;
 using hobf::FormatEntry;
+using hobf::xrec_of;
 
 #define HOBF_DECLARE(TAG)                                                                    \
   cudaError_t hobf_launch_conv_##TAG(const hobf::ConvArgs& a, cudaStream_t s);               \
@@ -231,11 +233,6 @@ __device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int wfo, int rn
 // 2^wF + 0/1/2 for zero/inf/NaN; padding = +0 -> row 2^wF).  One thread per
 // padded pixel, looping over the channels; consecutive threads write
 // consecutive columns (coalesced).
-__device__ __forceinline__ uint32_t xrec_of(uint32_t x, int we, int wf) {
-  const uint32_t exc = (x >> (wf + we + 1)) & 3u;
-  const uint32_t row = exc == 1u ? (x & ((1u << wf) - 1u)) : ((1u << wf) + (exc == 0u ? 0u : exc - 1u));
-  return x | (row << 20);
-}
 
 __global__ void __launch_bounds__(256) prepare_acts_kernel(const uint32_t* __restrict__ planes, int n, int h, int w,
                                                            int cin, int pad, int we, int wf,
@@ -455,9 +452,29 @@ hobf_status hobf_unpack_f32(int32_t we, int32_t wf, const uint32_t* d_planes, in
   return unpack_common(true, we, wf, d_planes, rows, c, d_x, stream);
 }
 
+// Epilogue arguments (hobf_epilogue) -> ConvArgs; HOBF_EINVAL if inconsistent.
+static bool set_epilogue(ConvArgs& a, hobf_fmt f, hobf_epilogue ep, bool records_ok) {
+  a.out_mode = ep.mode;
+  a.next_wf = ep.next_wf;
+  a.next_pad = ep.next_pad;
+  if (ep.mode == HOBF_OUT_PLANES) return true;
+  if (ep.next_wf < 1 || ep.next_pad < 0) return false;
+  if (ep.mode == HOBF_OUT_NEXT_PLANES) return 3 + f.we + ep.next_wf <= 32;
+  if (ep.mode == HOBF_OUT_NEXT_RECORDS) return records_ok && ep.next_wf <= kTabMaxWf && 3 + f.we + ep.next_wf <= 20;
+  return false;
+}
+
 hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
                         const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
                         int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
+  const hobf_epilogue ep = {HOBF_OUT_PLANES, 0, 0};
+  return hobf_conv2d_ex(f, d_x_planes, n, h, w, cin, d_w_planes, kh, kw, cout, stride, pad, relu, ep, d_y_planes,
+                        stream);
+}
+
+hobf_status hobf_conv2d_ex(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
+                           const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
+                           int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_y_planes, hobf_stream stream) {
   g_last_launches = 0;
   if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
     return HOBF_EINVAL;
@@ -477,6 +494,7 @@ hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
   a.variant = 0;
+  if (!set_epilogue(a, f, ep, false)) return HOBF_EINVAL;
   a.one = 1;
   a.two = 2u;
   if (e->conv(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
@@ -594,14 +612,15 @@ hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, i
 hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w, int32_t cin,
                                  const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
                                  int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
-  return hobf_conv2d_prepared_variant(f, d_xrec, n, h, w, cin, d_wtab, kh, kw, cout, stride, pad, relu, d_y_planes,
-                                      conv_tab_variant(), stream);
+  const hobf_epilogue ep = {HOBF_OUT_PLANES, 0, 0};
+  return hobf_conv2d_prepared_ex(f, d_xrec, n, h, w, cin, d_wtab, kh, kw, cout, stride, pad, relu, ep, d_y_planes,
+                                 conv_tab_variant(), stream);
 }
 
-hobf_status hobf_conv2d_prepared_variant(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
-                                         int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw,
-                                         int32_t cout, int32_t stride, int32_t pad, int32_t relu,
-                                         uint32_t* d_y_planes, int32_t variant, hobf_stream stream) {
+hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
+                                    int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout,
+                                    int32_t stride, int32_t pad, int32_t relu, hobf_epilogue ep,
+                                    uint32_t* d_y_planes, int32_t variant, hobf_stream stream) {
   const uint32_t* d_x_planes = d_xrec;
   g_last_launches = 0;
   if (variant != 0 && (variant < 3 || variant > 6)) return HOBF_EINVAL;
@@ -623,6 +642,7 @@ hobf_status hobf_conv2d_prepared_variant(hobf_fmt f, const uint32_t* d_xrec, int
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
   a.variant = variant;
+  if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;
   a.row_mul = 1u << 12;
   for (int j = 0; j < 32; j++) a.lift[j] = 1u << (31 - j);
   a.one = 1;

@@ -12,6 +12,10 @@ struct ConvArgs {
   int n, h, w, cin, kh, kw, cout, stride, pad, relu, ho, wo;
   int64_t items;       // n * ho * wo * ceil(cout/32)
   int variant;         // kernel variant (0 = auto)
+  int out_mode;        // 0: y = output planes F(we, wfo) [pix][G][NPO]
+                       // 1: y = planes of the next layer's F(we, next_wf) [pix][G][roundup(3+we+next_wf, 4)]
+                       // 2: y = next layer's activation records, F(we, next_wf), [n][cout][ho+2np][wo+2np]
+  int next_wf, next_pad;
   int one;             // always 1 (opaque to the compiler, see bcast_bit)
   unsigned two;        // always 2 (see bit01)
   unsigned row_mul;    // 2^12: IMAD.HI(rec, row_mul) = rec >> 20 (table row of an activation record)

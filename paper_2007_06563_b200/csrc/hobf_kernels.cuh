@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include "hobf_internal.h"
+#include "hobf_words.cuh"
 
 namespace hobf {
 
@@ -48,6 +49,81 @@ struct TapIter {
 // Bit b of w as 0/1, on the FMA pipe: high word of (w * 2^(31-b)) * two, two = 2.
 __device__ __forceinline__ uint32_t bit01(uint32_t w, uint32_t lift, uint32_t two) {
   return __umulhi(w * lift, two);
+}
+
+// ---------------------------------------------------------------------------
+// Output epilogue shared by the conv kernels.  acc holds the canonical (and,
+// if requested, ReLU'd) accumulator planes of output pixel pix (image ni, row
+// oy, column ox), channels 32g + lane.
+//   out_mode 0: the planes as they are, F(we, wfo) (NPO words, uint4 stores);
+//   out_mode 1: every lane re-rounded into the next layer's F(we, next_wf)
+//               (requant_word) and bitsliced again: the next layer's
+//               input planes, no unpack in between;
+//   out_mode 2: the same words written as the next layer's activation
+//               records (zero-padded by next_pad; the caller's buffer holds
+//               the +0 border), one coalesced 4-byte store per channel.
+// ---------------------------------------------------------------------------
+template <class F>
+__device__ __forceinline__ uint32_t lane_word(const uint32_t* acc, int l) {
+  uint32_t x = 0u;
+#pragma unroll
+  for (int j = 0; j < F::NOUT; j++) x |= ((acc[j] >> l) & 1u) << j;
+  return x;
+}
+
+template <class F>
+__device__ __forceinline__ void store_requant(const uint32_t* acc, const ConvArgs& a, int64_t pix, int g, int ni,
+                                           int oy, int ox) {
+  const int G = (a.cout + 31) >> 5;
+  const int nbn = 3 + F::WE + a.next_wf;
+  if (a.out_mode == 1) {
+    uint32_t P[32];
+#pragma unroll
+    for (int j = 0; j < 32; j++) P[j] = 0u;
+#pragma unroll 1
+    for (int l = 0; l < 32; l++) {
+      if (32 * g + l >= a.cout) break;  // padding lanes stay +0 (all planes zero)
+      const uint32_t w = requant_word(lane_word<F>(acc, l), F::WE, F::WFO, a.next_wf, F::RND);
+#pragma unroll
+      for (int j = 0; j < 32; j++) P[j] |= ((w >> j) & 1u) << l;
+    }
+    const int npn = (nbn + 3) / 4 * 4;
+    uint4* py = reinterpret_cast<uint4*>(a.y + (pix * G + g) * npn);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if (4 * q >= npn) break;
+      py[q] = make_uint4(P[4 * q], P[4 * q + 1], P[4 * q + 2], P[4 * q + 3]);
+    }
+  } else {
+    const int Hn = a.ho + 2 * a.next_pad, Wn = a.wo + 2 * a.next_pad;
+    uint32_t* base = a.y + (((int64_t)ni * a.cout + 32 * g) * Hn + oy + a.next_pad) * Wn + ox + a.next_pad;
+#pragma unroll 1
+    for (int l = 0; l < 32; l++) {
+      if (32 * g + l >= a.cout) break;
+      const uint32_t w = requant_word(lane_word<F>(acc, l), F::WE, F::WFO, a.next_wf, F::RND);
+      base[(int64_t)l * Hn * Wn] = xrec_of(w, F::WE, a.next_wf);
+    }
+  }
+}
+
+template <class F>
+__device__ __forceinline__ void store_out(const uint32_t* acc, const ConvArgs& a, int64_t pix, int g, int ni, int oy,
+                                          int ox) {
+  if (a.out_mode != 0) {
+    store_requant<F>(acc, a, pix, g, ni, oy, ox);
+    return;
+  }
+  const int G = (a.cout + 31) >> 5;
+  uint4* py = reinterpret_cast<uint4*>(a.y + (pix * G + g) * F::NPO);
+#pragma unroll
+  for (int q = 0; q < F::NPO / 4; q++) {
+    uint4 v;
+    v.x = (4 * q + 0 < F::NOUT) ? acc[(4 * q + 0) % F::NOUT] : 0u;
+    v.y = (4 * q + 1 < F::NOUT) ? acc[(4 * q + 1) % F::NOUT] : 0u;
+    v.z = (4 * q + 2 < F::NOUT) ? acc[(4 * q + 2) % F::NOUT] : 0u;
+    v.w = (4 * q + 3 < F::NOUT) ? acc[(4 * q + 3) % F::NOUT] : 0u;
+    py[q] = v;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -112,16 +188,7 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
     }
   }
   if (a.relu) F::relu(acc, acc);
-  uint4* py = reinterpret_cast<uint4*>(a.y + t * F::NPO);
-#pragma unroll
-  for (int q = 0; q < F::NPO / 4; q++) {
-    uint4 v;
-    v.x = (4 * q + 0 < F::NOUT) ? acc[(4 * q + 0) % F::NOUT] : 0u;
-    v.y = (4 * q + 1 < F::NOUT) ? acc[(4 * q + 1) % F::NOUT] : 0u;
-    v.z = (4 * q + 2 < F::NOUT) ? acc[(4 * q + 2) % F::NOUT] : 0u;
-    v.w = (4 * q + 3 < F::NOUT) ? acc[(4 * q + 3) % F::NOUT] : 0u;
-    py[q] = v;
-  }
+  store_out<F>(acc, a, pix, g, (int)ni, oy, ox);
 }
 
 // ---------------------------------------------------------------------------
@@ -259,16 +326,7 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   }
   F::canon(acc, acc);  // the chain keeps a relaxed accumulator (fpgen.build_mac_tab)
   if (a.relu) F::relu(acc, acc);
-  uint4* py = reinterpret_cast<uint4*>(a.y + (pix * G + g) * F::NPO);
-#pragma unroll
-  for (int q = 0; q < F::NPO / 4; q++) {
-    uint4 v;
-    v.x = (4 * q + 0 < F::NOUT) ? acc[(4 * q + 0) % F::NOUT] : 0u;
-    v.y = (4 * q + 1 < F::NOUT) ? acc[(4 * q + 1) % F::NOUT] : 0u;
-    v.z = (4 * q + 2 < F::NOUT) ? acc[(4 * q + 2) % F::NOUT] : 0u;
-    v.w = (4 * q + 3 < F::NOUT) ? acc[(4 * q + 3) % F::NOUT] : 0u;
-    py[q] = v;
-  }
+  store_out<F>(acc, a, pix, g, ni, oy, ox);
 }
 
 // mac_planes: acc[i] = add(acc[i], mul(a[i], b[i])) lane-wise on plane groups.

@@ -1,0 +1,50 @@
+// hobf_words.cuh -- per-element word helpers shared by the C-ABI kernels and the
+// per-format conv kernels: activation records and the layer-epilogue
+// re-rounding of a chained network.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hobf {
+
+// Activation record (hobf_prepare_activations, hobf_conv2d_prepared): the
+// canonical x word of F(we, wf) in bits [0, 20) and the weight-table row it
+// selects in bits [20, 32): row = frac for a normal x, 2^wF + 0/1/2 for
+// zero / inf / NaN (padding = +0 -> row 2^wF).
+__device__ __forceinline__ uint32_t xrec_of(uint32_t x, int we, int wf) {
+  const uint32_t exc = (x >> (wf + we + 1)) & 3u;
+  const uint32_t row = exc == 1u ? (x & ((1u << wf) - 1u)) : ((1u << wf) + (exc == 0u ? 0u : exc - 1u));
+  return x | (row << 20);
+}
+
+// Layer epilogue of a chained network ("rounding ... dealt with at the
+// end of the layer in the activation function", P:265 layers kept in the
+// custom format): a canonical word of F(we, wfi) re-rounded into the next
+// layer's F(we, wfo), RNE (ties to even) or RTZ.  The exponent width is
+// unchanged, so a normal stays normal unless rounding up leaves the top binade
+// (-> inf, L5); widening (wfo >= wfi) is exact; zero / inf keep
+// their sign, NaN stays the canonical NaN.
+__device__ __forceinline__ uint32_t requant_word(uint32_t x, int we, int wfi, int wfo, int rnd) {
+  const uint32_t exc = (x >> (wfi + we + 1)) & 3u;
+  const uint32_t s = (x >> (wfi + we)) & 1u;
+  const int top = wfo + we + 1;
+  if (exc != 1u) return (exc << top) | ((exc == 3u ? 0u : s) << (wfo + we));
+  uint32_t e = (x >> wfi) & ((1u << we) - 1u);
+  uint32_t f = x & ((1u << wfi) - 1u);
+  if (wfo >= wfi) {
+    f <<= (wfo - wfi);
+  } else {
+    const int sh = wfi - wfo;
+    const uint32_t rem = f & ((1u << sh) - 1u), half = 1u << (sh - 1);
+    f >>= sh;
+    if (rnd == 0 && (rem > half || (rem == half && (f & 1u)))) {
+      if (++f == (1u << wfo)) {  // carried into the next binade
+        f = 0u;
+        if (++e == (1u << we)) return (2u << top) | (s << (wfo + we));  // overflow -> inf
+      }
+    }
+  }
+  return (1u << top) | (s << (wfo + we)) | (e << wfo) | f;
+}
+
+}  // namespace hobf

@@ -38,6 +38,26 @@ class hobf_fmt(ctypes.Structure):
     _fields_ = [("we", ctypes.c_int32), ("wf", ctypes.c_int32), ("round", ctypes.c_int32), ("extended", ctypes.c_int32)]
 
 
+class hobf_epilogue(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("next_wf", ctypes.c_int32), ("next_pad", ctypes.c_int32)]
+
+
+OUT_PLANES, OUT_NEXT_PLANES, OUT_NEXT_RECORDS = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class Next:
+    """Layer-chaining epilogue (hobf_epilogue): write the output re-rounded into the
+    next layer's F(we, wf) as planes (records=False, for hobf_conv2d) or as
+    activation records padded by `pad` (records=True, for hobf_conv2d_prepared)."""
+    wf: int
+    records: bool = True
+    pad: int = 1
+
+    def c(self) -> hobf_epilogue:
+        return hobf_epilogue(OUT_NEXT_RECORDS if self.records else OUT_NEXT_PLANES, self.wf, self.pad)
+
+
 @dataclass(frozen=True)
 class Fmt:
     """Input format F(we, wf) plus MAC mode (round: 0 RNE / 1 RTZ; extended: 0 single)."""
@@ -91,9 +111,12 @@ _lib.hobf_prepare_weights.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, 
 _lib.hobf_conv2d_prepared.restype = _i32
 _lib.hobf_conv2d_prepared.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _i32,
                                       _p, _p]
-_lib.hobf_conv2d_prepared_variant.restype = _i32
-_lib.hobf_conv2d_prepared_variant.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32,
-                                              _i32, _p, _i32, _p]
+_lib.hobf_conv2d_prepared_ex.restype = _i32
+_lib.hobf_conv2d_prepared_ex.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32,
+                                         _i32, hobf_epilogue, _p, _i32, _p]
+_lib.hobf_conv2d_ex.restype = _i32
+_lib.hobf_conv2d_ex.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _i32,
+                                hobf_epilogue, _p, _p]
 _lib.hobf_xrec_words.restype = _i64
 _lib.hobf_xrec_words.argtypes = [_i32, _i32, _i32, _i32, _i32]
 _lib.hobf_prepare_activations.restype = _i32
@@ -110,7 +133,7 @@ _lib.hobf_version.restype = ctypes.c_char_p
 SYMBOLS = ["hobf_nbits", "hobf_out_wf", "hobf_nplanes", "hobf_planes_words", "hobf_pack", "hobf_quantize_pack",
            "hobf_unpack", "hobf_unpack_f32", "hobf_conv2d", "hobf_mac_planes", "hobf_gate_count",
            "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version",
-           "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_conv2d_prepared_variant", "hobf_xrec_words",
+           "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_conv2d_prepared_ex", "hobf_conv2d_ex", "hobf_xrec_words",
            "hobf_prepare_activations", "hobf_quantize_activations"]
 
 
@@ -199,15 +222,33 @@ def conv_out_hw(h, w, kh, kw, stride, pad):
     return (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
 
 
+def _next_out(f: Fmt, nxt, n, ho, wo, cout, device, out):
+    """Output buffer of a conv with epilogue `nxt` (None = plain output planes)."""
+    if nxt is None:
+        return _new_planes(max(n * ho * wo, 0), cout, f.nout, device, out)
+    if not nxt.records:
+        return _new_planes(max(n * ho * wo, 0), cout, nbits(f.we, nxt.wf), device, out)
+    if out is None:  # the +0 border of the next layer's records: (2^wf) << 20
+        out = torch.full((max(xrec_words(n, ho, wo, cout, nxt.pad), 4),), ((1 << nxt.wf) << 20),
+                         dtype=torch.int32, device=device)
+    return out
+
+
 def conv2d(f: Fmt, x_planes: torch.Tensor, n: int, h: int, w: int, cin: int, w_planes: torch.Tensor,
            kh: int, kw: int, cout: int, stride: int = 1, pad: int = 1, relu: int = 0, out=None,
-           stream=None) -> torch.Tensor:
-    """HOBFLOPS conv on planes; returns output planes [n*ho*wo, ceil(cout/32), NP(NOUT)]."""
+           stream=None, nxt: "Next | None" = None) -> torch.Tensor:
+    """HOBFLOPS conv on planes; returns output planes [n*ho*wo, ceil(cout/32), NP(NOUT)],
+    or with nxt = Next(wf, records=False) the next layer's input planes of F(we, wf)
+    (hobf_conv2d_ex, fused re-rounding epilogue)."""
     ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
-    dev = x_planes.device
-    out = _new_planes(max(n * ho * wo, 0), cout, f.nout, dev, out)
-    _check("hobf_conv2d", _lib.hobf_conv2d(f.c(), _ptr(x_planes), n, h, w, cin, _ptr(w_planes), kh, kw, cout,
-                                           stride, pad, int(relu), _ptr(out), _stream(stream)))
+    out = _next_out(f, nxt, n, ho, wo, cout, x_planes.device, out)
+    if nxt is None:
+        _check("hobf_conv2d", _lib.hobf_conv2d(f.c(), _ptr(x_planes), n, h, w, cin, _ptr(w_planes), kh, kw, cout,
+                                               stride, pad, int(relu), _ptr(out), _stream(stream)))
+    else:
+        _check("hobf_conv2d_ex", _lib.hobf_conv2d_ex(f.c(), _ptr(x_planes), n, h, w, cin, _ptr(w_planes), kh, kw,
+                                                     cout, stride, pad, int(relu), nxt.c(), _ptr(out),
+                                                     _stream(stream)))
     return out
 
 
@@ -269,20 +310,22 @@ def quantize_activations(f: Fmt, x: torch.Tensor, pad: int, out=None, stream=Non
 
 def conv2d_prepared(f: Fmt, xrec: torch.Tensor, n: int, h: int, w: int, cin: int, wtab: torch.Tensor,
                     kh: int, kw: int, cout: int, stride: int = 1, pad: int = 1, relu: int = 0, out=None,
-                    stream=None, variant: int | None = None) -> torch.Tensor:
+                    stream=None, variant: int | None = None, nxt: "Next | None" = None) -> torch.Tensor:
     """Conv on prepared activations (same pad) and prepared weights -> output planes.
-    variant: None = hobf_conv2d_prepared (automatic schedule), else
-    hobf_conv2d_prepared_variant with that kernel schedule (identical results)."""
+    variant: None = automatic kernel schedule, else that schedule (identical results);
+    nxt: Next(wf, records=True, pad) writes the next layer's activation records
+    (or planes) of F(we, wf) instead (hobf_conv2d_prepared_ex, fused re-rounding)."""
     ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
-    out = _new_planes(max(n * ho * wo, 0), cout, f.nout, xrec.device, out)
-    if variant is None:
+    out = _next_out(f, nxt, n, ho, wo, cout, xrec.device, out)
+    if variant is None and nxt is None:
         _check("hobf_conv2d_prepared", _lib.hobf_conv2d_prepared(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw,
                                                                  cout, stride, pad, int(relu), _ptr(out),
                                                                  _stream(stream)))
     else:
-        _check("hobf_conv2d_prepared_variant",
-               _lib.hobf_conv2d_prepared_variant(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw, cout, stride,
-                                                 pad, int(relu), _ptr(out), int(variant), _stream(stream)))
+        ep = nxt.c() if nxt is not None else hobf_epilogue(OUT_PLANES, 0, 0)
+        _check("hobf_conv2d_prepared_ex",
+               _lib.hobf_conv2d_prepared_ex(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw, cout, stride,
+                                            pad, int(relu), ep, _ptr(out), int(variant or 0), _stream(stream)))
     return out
 
 

@@ -419,3 +419,56 @@ def test_mac_random_extended(we, wf, rnd):
     got = run_mac(f, A, X, W)
     exp = oracle.mac(A, X, W, we, wf, f.wfo, rnd)
     assert np.array_equal(got, exp)
+
+
+# ----------------------------------------------------------------------------- layer chaining
+
+@pytest.mark.parametrize("prepared", [False, True])
+@pytest.mark.parametrize("we,wf1,wf2,ext,rnd", [(5, 3, 3, 0, 0), (5, 10, 3, 0, 0), (4, 3, 3, 1, 0), (5, 3, 3, 0, 1),
+                                                (6, 2, 5, 0, 0), (5, 4, 2, 1, 1)])
+def test_two_layer_chain_vs_oracle(prepared, we, wf1, wf2, ext, rnd):
+    """conv -> ReLU -> re-round into the next layer's format (fused epilogue) ->
+    conv, with no unpack in between, equals oracle.conv_chain word for word; the
+    intermediate (next-layer) tensor also equals oracle.convert of layer 1."""
+    H = hobf()
+    n, h, w, c0, c1, c2 = 2, 9, 11, 20, 40, 33
+    x, w1 = inputs.small_case(61, n, h, w, c0, c1, "normal", 0.4)
+    _, w2 = inputs.small_case(62, 1, 3, 3, c1, c2, "normal", 0.3)
+    x[0, 0, :2, 0] = [np.inf, -0.0]
+    f1, f2 = H.Fmt(we, wf1, rnd, extended=ext), H.Fmt(we, wf2, rnd)
+    xq = oracle.encode_f32(x, we, wf1, rnd)
+    w1q, w2q = oracle.encode_f32(w1, we, wf1, rnd), oracle.encode_f32(w2, we, wf2, rnd)
+    exp = oracle.conv_chain(xq, [(w1q, wf1, 1, 1, 1, ext), (w2q, wf2, 2, 1, 0, 0)], we, rnd)
+    mid = oracle.convert(oracle.conv2d(xq, w1q, we, wf1, f1.wfo, rnd, 1, 1, 1), we, f1.wfo, wf2, rnd)
+    wp1 = H.quantize_pack(we, wf1, torch.from_numpy(w1.reshape(-1, c1)).cuda(), rnd)
+    wp2 = H.quantize_pack(we, wf2, torch.from_numpy(w2.reshape(-1, c2)).cuda(), rnd)
+    ho2, wo2 = H.conv_out_hw(h, w, 3, 3, 2, 1)
+    if prepared and H.wtab_words(f1, 3, 3, c0, c1) > 0:
+        xr = H.quantize_activations(f1, torch.from_numpy(x).cuda(), 1)
+        t1, t2 = H.prepare_weights(f1, wp1, 3, 3, c0, c1), H.prepare_weights(f2, wp2, 3, 3, c1, c2)
+        r2 = H.conv2d_prepared(f1, xr, n, h, w, c0, t1, 3, 3, c1, 1, 1, 1, nxt=H.Next(wf2, records=True, pad=1))
+        # the records' words are the next layer's input: compare them with the oracle's conversion
+        rec = to_np_words(r2).reshape(n, c1, h + 2, w + 2)
+        got_mid = (rec[:, :, 1:-1, 1:-1] & 0xFFFFF).transpose(0, 2, 3, 1)
+        assert np.array_equal(got_mid, mid)
+        assert np.all((rec[:, :, 0, :] >> 20) == (1 << wf2)) and np.all((rec[:, :, :, 0] & 0xFFFFF) == 0)
+        yp = H.conv2d_prepared(f2, r2, n, h, w, c1, t2, 3, 3, c2, 2, 1, 0)
+    else:
+        xp = H.quantize_pack(we, wf1, torch.from_numpy(x.reshape(-1, c0)).cuda(), rnd)
+        p2 = H.conv2d(f1, xp, n, h, w, c0, wp1, 3, 3, c1, 1, 1, 1, nxt=H.Next(wf2, records=False))
+        got_mid = to_np_words(H.unpack(we, wf2, p2, n * h * w, c1)).reshape(mid.shape)
+        assert np.array_equal(got_mid, mid)
+        yp = H.conv2d(f2, p2, n, h, w, c1, wp2, 3, 3, c2, 2, 1, 0)
+    got = to_np_words(H.unpack(we, f2.wfo, yp, n * ho2 * wo2, c2)).reshape(exp.shape)
+    assert np.array_equal(got, exp), np.argwhere(got != exp)[:5]
+
+
+def test_chain_epilogue_argument_errors():
+    H = hobf()
+    f = H.Fmt(5, 3, 0)
+    xr = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    t = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
+    for nxt in (H.Next(0, True, 1), H.Next(3, True, -1), H.Next(12, True, 1), H.Next(30, False)):
+        out = torch.zeros(4096, dtype=torch.int32, device="cuda") if nxt.records else None
+        with pytest.raises(H.HobfError):
+            H.conv2d_prepared(f, xr, 1, 4, 4, 4, t, 3, 3, 8, 1, 1, 0, out=out, nxt=nxt)
