@@ -65,6 +65,8 @@ def lib():
         L.ref_conv2d.restype = i32
         L.ref_conv2d.argtypes = [P, i32, i32, i32, i32, P, i32, i32, i32,
                                  i32, i32, i32, i32, i32, i32, i32, P, i32]
+        L.ref_conv2d_dw.restype = i32
+        L.ref_conv2d_dw.argtypes = [P, i32, i32, i32, i32, P, i32, i32, i32, i32, i32, i32, i32, i32, i32, P, i32]
         L.ref_conv2d_sample.restype = i32
         L.ref_conv2d_sample.argtypes = [P, i32, i32, i32, i32, P, i32, i32, i32,
                                         i32, i32, i32, i32, i32, i32, i32, P, i64, P]
@@ -177,6 +179,22 @@ def conv2d(x, wts, we, wf, wf_out, mode=RNE, stride=1, pad=1, relu=0, nthreads=N
                           stride, pad, int(relu), we, wf, wf_out, mode, _ptr(y), int(nthreads))
     if rc != 0:
         raise ValueError("ref_conv2d: bad arguments")
+    return y
+
+
+def conv2d_dw(x, wts, we, wf, wf_out, mode=RNE, stride=1, pad=1, relu=0, nthreads=None) -> np.ndarray:
+    """Depthwise conv (ref_conv2d_dw): x [n,h,w,c] words, wts [kh,kw,c] words ->
+    [n,ho,wo,c] words in F(we, wf_out)."""
+    x, wts = _u32(x), _u32(wts)
+    n, h, w, c = x.shape
+    kh, kw, c2 = wts.shape
+    assert c2 == c
+    ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
+    y = np.empty((n, ho, wo, c), dtype=np.uint32)
+    nt = nthreads or os.cpu_count() or 1
+    rc = lib().ref_conv2d_dw(_ptr(x), n, h, w, c, _ptr(wts), kh, kw, stride, pad, relu, we, wf, wf_out, mode,
+                             _ptr(y), nt)
+    assert rc == 0
     return y
 
 

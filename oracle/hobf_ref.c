@@ -339,6 +339,61 @@ int ref_conv2d(const uint32_t* x, int n, int h, int wd, int cin,
     return 0;
 }
 
+/* ---------------- depthwise conv2d (the MobileNets
+ * "Conv dw / s2" layer of P:255 / P:270 in its depthwise form) ----------------
+ * x: NHWC words, C channels; w: [kh][kw][C] words (one kh x kw filter per
+ * channel); y: [n][ho][wo][C].  For every output (n, oy, ox, m):
+ *   acc = +0; for kh, for kw: acc = add(acc, mul(x[n, iy, ix, m] or +0, w[kh, kw, m]))
+ *   y = relu ? relu(acc) : acc            (same MAC, order and padding rules as conv2d) */
+static uint32_t conv_dw_one(const conv_job_t* J, int ni, int oy, int ox, int m) {
+    uint32_t acc = enc_special(CLS_ZERO, 0, J->we, J->wf_out);
+    const uint32_t pad_word = enc_special(CLS_ZERO, 0, J->we, J->wf);
+    for (int a = 0; a < J->kh; a++)
+        for (int b = 0; b < J->kw; b++) {
+            int iy = oy * J->stride - J->pad + a;
+            int ix = ox * J->stride - J->pad + b;
+            uint32_t xv = pad_word;
+            if (iy >= 0 && iy < J->h && ix >= 0 && ix < J->wd)
+                xv = J->x[(((int64_t)ni * J->h + iy) * J->wd + ix) * J->cin + m];
+            uint32_t wv = J->w[((int64_t)a * J->kw + b) * J->cin + m];
+            acc = ref_add(acc, ref_mul(xv, wv, J->we, J->wf, J->wf_out, J->mode), J->we, J->wf_out, J->mode);
+        }
+    return J->relu ? ref_relu(acc, J->we, J->wf_out) : acc;
+}
+
+static void* conv_dw_worker(void* arg) {
+    conv_job_t* J = (conv_job_t*)arg;
+    for (int64_t p = J->lo; p < J->hi; p++) {
+        int ox = (int)(p % J->wo);
+        int oy = (int)((p / J->wo) % J->ho);
+        int ni = (int)(p / ((int64_t)J->wo * J->ho));
+        for (int m = 0; m < J->cin; m++) J->y[p * J->cin + m] = conv_dw_one(J, ni, oy, ox, m);
+    }
+    return NULL;
+}
+
+int ref_conv2d_dw(const uint32_t* x, int n, int h, int wd, int c, const uint32_t* w, int kh, int kw,
+                  int stride, int pad, int relu, int we, int wf, int wf_out, int mode,
+                  uint32_t* y, int nthreads) {
+    if (n < 0 || h <= 0 || wd <= 0 || c <= 0 || kh <= 0 || kw <= 0 || stride <= 0 || pad < 0) return -1;
+    int ho = (h + 2 * pad - kh) / stride + 1, wo = (wd + 2 * pad - kw) / stride + 1;
+    if (ho <= 0 || wo <= 0) return -1;
+    int64_t npix = (int64_t)n * ho * wo;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    conv_job_t jobs[256];
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; t++) {
+        conv_job_t J = {x, w, y, n, h, wd, c, kh, kw, c, stride, pad, relu, we, wf, wf_out, mode,
+                        ho, wo, npix * t / nthreads, npix * (t + 1) / nthreads};
+        jobs[t] = J;
+    }
+    if (nthreads == 1) { conv_dw_worker(&jobs[0]); return 0; }
+    for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, conv_dw_worker, &jobs[t]);
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    return 0;
+}
+
 /* Sampled outputs at full size: idx[i] = ((ni*ho + oy)*wo + ox)*cout + m. */
 int ref_conv2d_sample(const uint32_t* x, int n, int h, int wd, int cin,
                       const uint32_t* w, int kh, int kw, int cout,

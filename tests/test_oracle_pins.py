@@ -465,3 +465,49 @@ def test_conv_chain_is_layerwise():
     y = oracle.conv_chain(x, [(w1, wf, 1, 1, 1, 0), (ident, wf, 1, 1, 0, 0)], we)
     y1 = oracle.convert(oracle.conv2d(x, w1, we, wf, wf + 1, 0, 1, 1, 1), we, wf + 1, wf)
     assert np.array_equal(oracle.decode_f64(y, we, wf + 1), oracle.decode_f64(y1, we, wf))
+
+
+# ----------------------------------------------------------------------------- depthwise conv (MobileNets Conv dw)
+
+@pytest.mark.parametrize("stride", [1, 2])
+def test_conv_dw_vs_rational(stride):
+    """ref_conv2d_dw against an exact-rational chain of pyref.mul / pyref.add over
+    (kh, kw) on a tiny case with ragged spatial size and zero padding."""
+    we, wf, mode = 4, 3, 0
+    rng = np.random.default_rng(11)
+    x = oracle.encode_f32(rng.standard_normal((1, 5, 4, 3)).astype(np.float32), we, wf)
+    wt = oracle.encode_f32((rng.standard_normal((3, 3, 3)) * 0.7).astype(np.float32), we, wf)
+    for relu in (0, 1):
+        got = oracle.conv2d_dw(x, wt, we, wf, wf + 1, mode, stride, 1, relu, nthreads=2)
+        ho, wo = got.shape[1:3]
+        for oy in range(ho):
+            for ox in range(wo):
+                for m in range(3):
+                    acc = 0
+                    for a in range(3):
+                        for b in range(3):
+                            iy, ix = oy * stride - 1 + a, ox * stride - 1 + b
+                            xv = int(x[0, iy, ix, m]) if 0 <= iy < 5 and 0 <= ix < 4 else 0
+                            acc = pyref.add(acc, pyref.mul(xv, int(wt[a, b, m]), we, wf, wf + 1, mode), we, wf + 1, mode)
+                    if relu:
+                        acc = pyref.relu(acc, we, wf + 1)
+                    assert int(got[0, oy, ox, m]) == acc, (oy, ox, m)
+
+
+def test_conv_dw_equals_full_conv_with_diagonal_kernel():
+    """For finite inputs a depthwise conv is the full conv whose kernel is zero off
+    the channel diagonal: the extra products are +-0, and acc + (+-0) = acc for
+    every accumulator the chain can hold (+0, normals; L7), in the same relative
+    (kh, kw) order -- so the pinned full conv pins the depthwise one."""
+    we, wf = 5, 10
+    rng = np.random.default_rng(12)
+    n, h, w, c = 2, 7, 6, 9
+    x = oracle.encode_f32(rng.standard_normal((n, h, w, c)).astype(np.float32), we, wf)
+    wt = oracle.encode_f32((rng.standard_normal((3, 3, c)) * 0.5).astype(np.float32), we, wf)
+    full = np.zeros((3, 3, c, c), dtype=np.uint32)
+    for m in range(c):
+        full[:, :, m, m] = wt[:, :, m]
+    for stride, relu in ((1, 0), (2, 1)):
+        a = oracle.conv2d_dw(x, wt, we, wf, wf + 1, 0, stride, 1, relu)
+        b = oracle.conv2d(x, full, we, wf, wf + 1, 0, stride, 1, relu)
+        assert np.array_equal(a, b)
