@@ -183,11 +183,12 @@ def run_reference(a, dist):
     wq = oracle.encode_f32(w, we, wf, rnd)
     xin = np.ascontiguousarray(xq[:, :rows])
     ho_s = (rows + 2 * cfg.pad - cfg.kh) // cfg.stride + 1
-    sample_macs = ho_s * cfg.wo * cfg.cout * cfg.cin * cfg.kh * cfg.kw
+    sample_macs = ho_s * cfg.wo * cfg.cout * (1 if cfg.dw else cfg.cin) * cfg.kh * cfg.kw
+    conv = oracle.conv2d_dw if cfg.dw else oracle.conv2d
 
     def step():
         wfo = 2 * wf + 1 if a.extended else wf + 1
-        y = oracle.conv2d(xin, wq, we, wf, wfo, rnd, cfg.stride, cfg.pad, a.relu, nthreads=cores)
+        y = conv(xin, wq, we, wf, wfo, rnd, cfg.stride, cfg.pad, a.relu, nthreads=cores)
         return y
 
     for _ in range(a.warmup):
@@ -220,7 +221,8 @@ def cpu_baseline(cfg, we, wf, wfo, rnd, relu, target_macs):
     xq = oracle.encode_f32(x, we, wf, rnd)
     wq = oracle.encode_f32(w, we, wf, rnd)
     t0 = time.perf_counter()
-    oracle.conv2d(xq, wq, we, wf, wfo, rnd, cfg.stride, cfg.pad, relu, nthreads=cores)
+    conv = oracle.conv2d_dw if cfg.dw else oracle.conv2d
+    conv(xq, wq, we, wf, wfo, rnd, cfg.stride, cfg.pad, relu, nthreads=cores)
     dt = time.perf_counter() - t0
     return {"value": cfg.macs(n) / dt, "unit": "MAC/s", "cores": cores, "kind": "oracle",
             "sample": f"{n} of {cfg.n} images of {cfg.name} (full conv, every output exact), {dt:.1f} s"}
@@ -232,7 +234,10 @@ def parity_sample(cfg, we, wf, wfo, rnd, relu, y_words, x_f32, w_f32, k=256):
     wq = oracle.encode_f32(w_f32, we, wf, rnd)
     rng = np.random.default_rng(123)
     idx = rng.integers(0, y_words.size, k)
-    exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wfo, rnd, cfg.stride, cfg.pad, relu)
+    if cfg.dw:
+        exp = oracle.conv2d_dw(xq, wq, we, wf, wfo, rnd, cfg.stride, cfg.pad, relu).ravel()[idx]
+    else:
+        exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wfo, rnd, cfg.stride, cfg.pad, relu)
     return {"checked": int(k), "mismatches": int((y_words.ravel()[idx] != exp).sum())}
 
 
@@ -250,11 +255,14 @@ def run_gpu(a, dist):
     f = H.Fmt(we, wf, rnd, extended=a.extended)
     n = cfg.n
     x_np, w_np = inputs.draw(cfg, n=n, shard=dist.rank)
-    rows_x, rows_w, rows_y = n * cfg.h * cfg.w, cfg.kh * cfg.kw * cfg.cin, n * cfg.ho * cfg.wo
+    rows_x, rows_y = n * cfg.h * cfg.w, n * cfg.ho * cfg.wo
+    rows_w = cfg.kh * cfg.kw * (1 if cfg.dw else cfg.cin)
     wt = torch.from_numpy(w_np.reshape(rows_w, cfg.cout)).to(dev)
     wp = torch.empty(H.planes_shape(rows_w, cfg.cout, f.nin), dtype=torch.int32, device=dev)
-    tab_words = H.wtab_words(f, cfg.kh, cfg.kw, cfg.cin, cfg.cout)
-    use_tab = a.kernel == "tables" or (a.kernel == "auto" and tab_words > 0)
+    tab_words = 0 if cfg.dw else H.wtab_words(f, cfg.kh, cfg.kw, cfg.cin, cfg.cout)
+    # depthwise: the activation is not broadcast (lanes = channels of both operands),
+    # so there is no weight table: the full gate MAC (hobf_conv2d_dw)
+    use_tab = not cfg.dw and (a.kernel == "tables" or (a.kernel == "auto" and tab_words > 0))
     wtab = torch.empty(max(tab_words, 4), dtype=torch.int32, device=dev) if use_tab else None
     # double-buffered per-step activations / outputs (the e2e leg overlaps copies with compute)
     xs = [torch.from_numpy(x_np).to(dev) for _ in range(2)]
@@ -282,6 +290,9 @@ def run_gpu(a, dist):
         if use_tab:
             H.conv2d_prepared(f, xrec, n, cfg.h, cfg.w, cfg.cin, wtab, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad,
                               a.relu, out=yp, stream=st)
+        elif cfg.dw:
+            H.conv2d_dw(f, xp, n, cfg.h, cfg.w, cfg.cin, wp, cfg.kh, cfg.kw, cfg.stride, cfg.pad, a.relu, out=yp,
+                        stream=st)
         else:
             H.conv2d(f, xp, n, cfg.h, cfg.w, cfg.cin, wp, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad, a.relu,
                      out=yp, stream=st)
@@ -411,6 +422,7 @@ def run_gpu(a, dist):
                    "mac_class": "extended" if a.extended else "single", "relu": a.relu, "global_batch": n * dist.world, "per_gpu_batch": n,
                    "dense_macs_per_step": macs_rank * dist.world, "l2": "flushed (256 MiB write) between timed steps",
                    "step": (("quantize_activations(x) + conv2d_prepared + unpack_f32(y)" if use_tab else
+                              "quantize_pack(x) + conv2d_dw + unpack_f32(y)" if cfg.dw else
                               "quantize_pack(x) + conv2d + unpack_f32(y)") +
                              (" + weight prep" if a.weights_per_step else
                               "; weights prepared once per layer (quantize_pack(w) + prepare_weights, P:203), "
@@ -419,7 +431,8 @@ def run_gpu(a, dist):
                    "parallelism": f"dp{dist.world} (batch shards, no collective)"},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlop3/s",
                      "frac": achieved / peak, "traffic": measured_traffic(cfg.name, we, wf, use_tab),
-                     "kernel": "conv2d_prepared (weight tables)" if use_tab else "conv2d (full lop3 MAC)",
+                     "kernel": "conv2d_prepared (weight tables)" if use_tab else
+                               "conv2d_dw (depthwise, full lop3 MAC)" if cfg.dw else "conv2d (full lop3 MAC)",
                      "gates_per_32lane_mac": G, "gates_full_mac": g["mac"],
                      "peak_source": f"derived: {N_SM} SM x {LOP3_PER_SM_CLK} lop3/clk x {sm_mhz:.0f} MHz",
                      "measured_lop3_peak": measured_peak / 1e12,

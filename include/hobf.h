@@ -188,6 +188,19 @@ hobf_status hobf_conv2d_ex(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
                            const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
                            int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_out, hobf_stream stream);
 
+/* Depthwise conv (MobileNets "Conv dw", the layer of P:255 / P:270; SURVEY
+ * 8(f) row 4): output channel m = serial (kh, kw) chain over input channel m
+ * only, acc = +0; acc = add(acc, mul(x[n, iy, ix, m] or +0, w[kh, kw, m])),
+ * same MAC, rounding, padding and ReLU rules as hobf_conv2d (oracle:
+ * ref_conv2d_dw).  The 32 lanes are 32 channels of both operands (no
+ * broadcast), so every lane runs the full gate MAC (hobf_gate_count mac).
+ * x planes: [n*h*w][ceil(c/32)][NP(NIN)]; w planes: [kh*kw][ceil(c/32)][NP(NIN)]
+ * (words [kh][kw][c]); output per `ep` as for hobf_conv2d_ex with cout = c
+ * (records: the next layer's prepared activations). */
+hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t c,
+                           const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                           int32_t relu, hobf_epilogue ep, uint32_t* d_out, hobf_stream stream);
+
 /* hobf_conv2d_prepared with an epilogue (above) and an explicit kernel
  * schedule: variant 0 = automatic (what hobf_conv2d_prepared uses; the
  * environment variable HOBF_CONV_VARIANT overrides it there), 3 = one thread

@@ -20,9 +20,11 @@ using hobf::xrec_of;
   cudaError_t hobf_launch_conv_##TAG(const hobf::ConvArgs& a, cudaStream_t s);               \
   cudaError_t hobf_launch_mac_##TAG(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n, \
                                     cudaStream_t s);                                         \
-  cudaError_t hobf_launch_convtab_##TAG(const hobf::ConvArgs& a, cudaStream_t s);
+  cudaError_t hobf_launch_convtab_##TAG(const hobf::ConvArgs& a, cudaStream_t s);            \
+  cudaError_t hobf_launch_convdw_##TAG(const hobf::ConvArgs& a, cudaStream_t s);
 #define HOBF_ENTRY(TAG, WE, WF, RND, EXT, GM, GMUL, GADD, GRELU, GTAB) \
-  {WE, WF, RND, EXT, GM, GMUL, GADD, GRELU, GTAB, hobf_launch_conv_##TAG, hobf_launch_mac_##TAG, hobf_launch_convtab_##TAG},
+  {WE, WF, RND, EXT, GM, GMUL, GADD, GRELU, GTAB, hobf_launch_conv_##TAG, hobf_launch_mac_##TAG, hobf_launch_convtab_##TAG, \
+   hobf_launch_convdw_##TAG},
 #include "gen/hobf_table.inc"
 
 static const FormatEntry kFormats[] = {HOBF_TABLE_ENTRIES};
@@ -498,6 +500,35 @@ hobf_status hobf_conv2d_ex(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
   a.one = 1;
   a.two = 2u;
   if (e->conv(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
+}
+
+hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t c,
+                           const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
+                           int32_t relu, hobf_epilogue ep, uint32_t* d_out, hobf_stream stream) {
+  g_last_launches = 0;
+  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
+    return HOBF_EINVAL;
+  if (n < 0 || h < 0 || w < 0 || c < 0 || kh < 0 || kw < 0 || stride <= 0 || pad < 0) return HOBF_EINVAL;
+  if (h == 0 || w == 0 || c == 0 || kh == 0 || kw == 0) return HOBF_ESHAPE;
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
+  const FormatEntry* e = find_format(f.we, f.wf, f.round, f.extended);
+  if (!e) return HOBF_EUNSUPPORTED;
+  if (n == 0) return HOBF_OK;
+  if (!d_x_planes || !d_w_planes || !d_out) return HOBF_EINVAL;
+  if (!aligned16(d_x_planes) || !aligned16(d_w_planes) || !aligned16(d_out)) return HOBF_EINVAL;
+  ConvArgs a;
+  a.x = d_x_planes; a.wt = d_w_planes; a.y = d_out;
+  a.n = n; a.h = h; a.w = w; a.cin = c; a.kh = kh; a.kw = kw; a.cout = c;
+  a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
+  a.items = (int64_t)n * ho * wo * ((c + 31) / 32);
+  a.variant = 0;
+  if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;
+  a.one = 1;
+  a.two = 2u;
+  if (e->conv_dw(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;
 }

@@ -30,6 +30,7 @@ struct FormatEntry {
   conv_launcher conv;
   mac_launcher mac;
   conv_launcher conv_tab;  // conv with the multiplier read from per-weight tables
+  conv_launcher conv_dw;   // depthwise conv (full MAC per lane)
 };
 
 }  // namespace hobf

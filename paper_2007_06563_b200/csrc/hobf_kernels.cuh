@@ -192,6 +192,55 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Depthwise conv2d (MobileNets "Conv dw"):
+// output channel m reads only input channel m, so the 32 lanes of a register
+// are 32 channels of BOTH operands -- the activation is bitsliced like the
+// weight (no broadcast) and every lane runs its own full MAC (F::mac: the
+// (wF+1)^2 multiplier array and the adder).  One thread = one output pixel x
+// one group of 32 channels; the serial (kh, kw) chain stays in registers.
+// x planes [n][h][w][G][NPI], w planes [kh][kw][G][NPI], G = ceil(C/32).
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(128) conv_dw_kernel(ConvArgs a) {
+  const int G = (a.cout + 31) >> 5;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.items) return;
+  const int g = (int)(t % G);
+  const int64_t pix = t / G;
+  const int ox = (int)(pix % a.wo);
+  const int oy = (int)((pix / a.wo) % a.ho);
+  const int ni = (int)(pix / ((int64_t)a.wo * a.ho));
+
+  uint32_t acc[F::NOUT];
+#pragma unroll
+  for (int j = 0; j < F::NOUT; j++) acc[j] = 0u;  // +0 (L9)
+  const uint32_t* __restrict__ xbase = a.x + ((int64_t)ni * a.h * a.w * G + g) * F::NPI;
+  const uint32_t* __restrict__ wbase = a.wt + (int64_t)g * F::NPI;
+#pragma unroll 1
+  for (int kh = 0; kh < a.kh; kh++) {
+    const int iy = oy * a.stride - a.pad + kh;
+#pragma unroll 1
+    for (int kw = 0; kw < a.kw; kw++) {
+      const int ix = ox * a.stride - a.pad + kw;
+      uint32_t X[F::NPI], W[F::NPI];
+      const bool inside = iy >= 0 && iy < a.h && ix >= 0 && ix < a.w;
+      const uint4* px = reinterpret_cast<const uint4*>(xbase + ((int64_t)iy * a.w + ix) * G * F::NPI);
+      const uint4* pw = reinterpret_cast<const uint4*>(wbase + (int64_t)(kh * a.kw + kw) * G * F::NPI);
+#pragma unroll
+      for (int q = 0; q < F::NPI / 4; q++) {
+        const uint4 v = inside ? __ldg(px + q) : make_uint4(0u, 0u, 0u, 0u);  // padding = +0 (L11, L14)
+        X[4 * q + 0] = v.x; X[4 * q + 1] = v.y; X[4 * q + 2] = v.z; X[4 * q + 3] = v.w;
+        const uint4 u = __ldg(pw + q);
+        W[4 * q + 0] = u.x; W[4 * q + 1] = u.y; W[4 * q + 2] = u.z; W[4 * q + 3] = u.w;
+      }
+      F::mac(acc, X, W);
+    }
+  }
+  if (a.relu) F::relu(acc, acc);
+  store_out<F>(acc, a, pix, g, ni, oy, ox);
+}
+
+// ---------------------------------------------------------------------------
 // conv2d with prepared weights and prepared activations.
 //
 // The activation x is one scalar per thread (broadcast across the 32
@@ -387,6 +436,14 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
 }
 
 template <class F>
+cudaError_t launch_conv_dw(const ConvArgs& a, cudaStream_t s) {
+  if (a.items == 0) return cudaSuccess;
+  const int threads = 128;
+  conv_dw_kernel<F><<<(unsigned)((a.items + threads - 1) / threads), threads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <class F>
 cudaError_t launch_mac(uint32_t* acc, const uint32_t* x, const uint32_t* w, int64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
@@ -407,4 +464,7 @@ cudaError_t launch_mac(uint32_t* acc, const uint32_t* x, const uint32_t* w, int6
   }                                                                                                         \
   cudaError_t hobf_launch_convtab_##TAG(const hobf::ConvArgs& a, cudaStream_t s) {                         \
     return hobf::launch_conv_tab<hobf_gen::F_##TAG>(a, s);                                                  \
+  }                                                                                                         \
+  cudaError_t hobf_launch_convdw_##TAG(const hobf::ConvArgs& a, cudaStream_t s) {                          \
+    return hobf::launch_conv_dw<hobf_gen::F_##TAG>(a, s);                                                   \
   }

@@ -114,6 +114,9 @@ _lib.hobf_conv2d_prepared.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, 
 _lib.hobf_conv2d_prepared_ex.restype = _i32
 _lib.hobf_conv2d_prepared_ex.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32,
                                          _i32, hobf_epilogue, _p, _i32, _p]
+_lib.hobf_conv2d_dw.restype = _i32
+_lib.hobf_conv2d_dw.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, hobf_epilogue,
+                                _p, _p]
 _lib.hobf_conv2d_ex.restype = _i32
 _lib.hobf_conv2d_ex.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _p, _i32, _i32, _i32, _i32, _i32, _i32,
                                 hobf_epilogue, _p, _p]
@@ -133,7 +136,7 @@ _lib.hobf_version.restype = ctypes.c_char_p
 SYMBOLS = ["hobf_nbits", "hobf_out_wf", "hobf_nplanes", "hobf_planes_words", "hobf_pack", "hobf_quantize_pack",
            "hobf_unpack", "hobf_unpack_f32", "hobf_conv2d", "hobf_mac_planes", "hobf_gate_count",
            "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version",
-           "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_conv2d_prepared_ex", "hobf_conv2d_ex", "hobf_xrec_words",
+           "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_conv2d_prepared_ex", "hobf_conv2d_ex", "hobf_conv2d_dw", "hobf_xrec_words",
            "hobf_prepare_activations", "hobf_quantize_activations"]
 
 
@@ -249,6 +252,19 @@ def conv2d(f: Fmt, x_planes: torch.Tensor, n: int, h: int, w: int, cin: int, w_p
         _check("hobf_conv2d_ex", _lib.hobf_conv2d_ex(f.c(), _ptr(x_planes), n, h, w, cin, _ptr(w_planes), kh, kw,
                                                      cout, stride, pad, int(relu), nxt.c(), _ptr(out),
                                                      _stream(stream)))
+    return out
+
+
+def conv2d_dw(f: Fmt, x_planes: torch.Tensor, n: int, h: int, w: int, c: int, w_planes: torch.Tensor,
+              kh: int, kw: int, stride: int = 1, pad: int = 1, relu: int = 0, out=None, stream=None,
+              nxt: "Next | None" = None) -> torch.Tensor:
+    """Depthwise conv (hobf_conv2d_dw): x planes [n*h*w, G, NP], w planes of the
+    [kh][kw][c] words -> output planes (or the next layer's planes / records, nxt)."""
+    ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
+    out = _next_out(f, nxt, n, ho, wo, c, x_planes.device, out)
+    ep = nxt.c() if nxt is not None else hobf_epilogue(OUT_PLANES, 0, 0)
+    _check("hobf_conv2d_dw", _lib.hobf_conv2d_dw(f.c(), _ptr(x_planes), n, h, w, c, _ptr(w_planes), kh, kw, stride,
+                                                 pad, int(relu), ep, _ptr(out), _stream(stream)))
     return out
 
 

@@ -35,6 +35,7 @@ class ConvConfig:
     stride: int = 1
     pad: int = 1
     text: str = ""
+    dw: bool = False         # depthwise: cout == cin, weights [kh, kw, cin]
 
     @property
     def ho(self):
@@ -47,6 +48,8 @@ class ConvConfig:
     def macs(self, n=None):
         """Dense MACs (padding taps counted, ledger L11)."""
         n = self.n if n is None else n
+        if self.dw:
+            return n * self.ho * self.wo * self.cout * self.kh * self.kw
         return n * self.ho * self.wo * self.cout * self.cin * self.kh * self.kw
 
 
@@ -63,6 +66,17 @@ CONFIGS = {
                      text="BASELINE configs[3]: 3x3 s1 p1, batch 256, 28x28x128 -> 128, e4m3 (HOBFLOPSIEEE8)"),
     "C5": ConvConfig("C5", 64, 14, 14, 256, 256, SWEEP, "uniform4", 0.05,
                      text="BASELINE configs[4]: format sweep e4-6 m2-10, 3x3 s1 p1, batch 64, 14x14x256 -> 256"),
+    # The paper's own workload shape: MobileNets
+    # "Conv dw / s2" at 14x14x512, stride 2 -- as the paper runs it (a full conv of
+    # M = 512 kernels over C = 512 channels, the IFM broadcast across the kernels,
+    # P:257) and in its depthwise form.  The paper states no value distribution:
+    # ReLU(N(0,1)) activations and He-normal weights like C2-C4; HOBFLOPS9 (e5m3).
+    "MOB": ConvConfig("MOB", 128, 14, 14, 512, 512, ((5, 3),), "relu_normal", math.sqrt(2 / (9 * 512)),
+                      stride=2, text="MobileNets Conv dw/s2 shape as a full conv (P:255): batch 128, 14x14x512 -> "
+                                     "7x7x512, 3x3 s2 p1, e5m3"),
+    "MOBDW": ConvConfig("MOBDW", 256, 14, 14, 512, 512, ((5, 3),), "relu_normal", math.sqrt(2 / 9),
+                        stride=2, dw=True, text="MobileNets Conv dw/s2, depthwise (P:255): batch 256, 14x14x512 -> "
+                                               "7x7x512, 3x3 s2 p1, e5m3"),
 }
 
 
@@ -71,7 +85,8 @@ def draw(cfg: ConvConfig, n: int | None = None, shard: int = 0, seed: int = 0):
     n = cfg.n if n is None else n
     rng = np.random.Generator(np.random.PCG64(seed))
     xs = _draw_x(rng, cfg, cfg.n)
-    wt = (rng.standard_normal((cfg.kh, cfg.kw, cfg.cin, cfg.cout), dtype=np.float32) * np.float32(cfg.w_sigma))
+    wshape = (cfg.kh, cfg.kw, cfg.cin) if cfg.dw else (cfg.kh, cfg.kw, cfg.cin, cfg.cout)
+    wt = (rng.standard_normal(wshape, dtype=np.float32) * np.float32(cfg.w_sigma))
     if shard == 0 and n == cfg.n:
         return xs, wt
     if shard == 0:
@@ -95,7 +110,7 @@ def _draw_x(rng, cfg: ConvConfig, n: int):
 
 
 def small_case(seed: int, n: int, h: int, w: int, cin: int, cout: int, dist: str = "normal",
-               w_sigma: float = 0.5, kh: int = 3, kw: int = 3):
+               w_sigma: float = 0.5, kh: int = 3, kw: int = 3, dw: bool = False):
     """Small seeded case for parity tests (several tiles + ragged tails)."""
-    cfg = ConvConfig("small", n, h, w, cin, cout, (), dist, w_sigma, kh, kw)
+    cfg = ConvConfig("small", n, h, w, cin, cout, (), dist, w_sigma, kh, kw, dw=dw)
     return draw(cfg, seed=seed)

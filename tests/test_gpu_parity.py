@@ -472,3 +472,79 @@ def test_chain_epilogue_argument_errors():
         out = torch.zeros(4096, dtype=torch.int32, device="cuda") if nxt.records else None
         with pytest.raises(H.HobfError):
             H.conv2d_prepared(f, xr, 1, 4, 4, 4, t, 3, 3, 8, 1, 1, 0, out=out, nxt=nxt)
+
+
+# ----------------------------------------------------------------------------- depthwise conv (MobileNets Conv dw)
+
+def gpu_conv_dw(x_f32, w_f32, f, stride=1, pad=1, relu=0, nxt=None):
+    H = hobf()
+    n, h, w, c = x_f32.shape
+    kh, kw, _ = w_f32.shape
+    xp = H.quantize_pack(f.we, f.wf, torch.from_numpy(x_f32.reshape(-1, c)).cuda(), f.round)
+    wp = H.quantize_pack(f.we, f.wf, torch.from_numpy(w_f32.reshape(-1, c)).cuda(), f.round)
+    yp = H.conv2d_dw(f, xp, n, h, w, c, wp, kh, kw, stride, pad, relu, nxt=nxt)
+    ho, wo = H.conv_out_hw(h, w, kh, kw, stride, pad)
+    if nxt is not None:
+        return yp, ho, wo
+    return to_np_words(H.unpack(f.we, f.wfo, yp, n * ho * wo, c)).reshape(n, ho, wo, c)
+
+
+@pytest.mark.parametrize("we,wf,ext", [(5, 3, 0), (4, 3, 0), (5, 10, 0), (6, 6, 0), (5, 3, 1), (4, 7, 1)])
+@pytest.mark.parametrize("stride", [1, 2])
+def test_conv_dw_vs_oracle(we, wf, ext, stride):
+    """Depthwise conv: ragged channel count (several 32-lane groups + tail), ragged
+    spatial tiles, specials, both rounding modes and ReLU settings."""
+    H = hobf()
+    x, w = inputs.small_case(71, 3, 13, 11, 75, 75, "normal", 0.5, dw=True)
+    x[0, 0, :3, 0] = [np.inf, np.nan, -0.0]
+    w[0, 1, :2] = [np.inf, 0.0]
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd, extended=ext)
+        xq, wq = oracle.encode_f32(x, we, wf, rnd), oracle.encode_f32(w, we, wf, rnd)
+        for relu in (0, 1):
+            exp = oracle.conv2d_dw(xq, wq, we, wf, f.wfo, rnd, stride, 1, relu)
+            got = gpu_conv_dw(x, w, f, stride, 1, relu)
+            assert np.array_equal(got, exp), (rnd, relu, np.argwhere(got != exp)[:5])
+
+
+def test_conv_dw_chain_into_pointwise_records():
+    """MobileNets block: depthwise 3x3 s2 -> ReLU -> re-round (fused epilogue) into
+    activation records -> full 1x1 conv on the weight-table path; equals the oracle."""
+    H = hobf()
+    we, wf = 5, 3
+    f = H.Fmt(we, wf, 0)
+    n, h, w, c, m = 2, 14, 14, 64, 96
+    x, wd = inputs.small_case(72, n, h, w, c, c, "relu_normal", 0.4, dw=True)
+    _, wpw = inputs.small_case(73, 1, 1, 1, c, m, "normal", 0.2, kh=1, kw=1)
+    rec, ho, wo = gpu_conv_dw(x, wd, f, 2, 1, 1, nxt=H.Next(wf, records=True, pad=0))
+    wp = H.quantize_pack(we, wf, torch.from_numpy(wpw.reshape(-1, m)).cuda(), 0)
+    tab = H.prepare_weights(f, wp, 1, 1, c, m)
+    yp = H.conv2d_prepared(f, rec, n, ho, wo, c, tab, 1, 1, m, 1, 0, 0)
+    got = to_np_words(H.unpack(we, f.wfo, yp, n * ho * wo, m)).reshape(n, ho, wo, m)
+    xq, wdq, wpq = (oracle.encode_f32(a, we, wf) for a in (x, wd, wpw))
+    mid = oracle.convert(oracle.conv2d_dw(xq, wdq, we, wf, wf + 1, 0, 2, 1, 1), we, wf + 1, wf)
+    exp = oracle.conv2d(mid, wpq, we, wf, wf + 1, 0, 1, 0, 0)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("name", ["MOB", "MOBDW"])
+def test_mobilenets_layer_sampled(name):
+    """The paper's layer shape at full size: sampled outputs vs the oracle."""
+    H = hobf()
+    cfg = inputs.CONFIGS[name]
+    we, wf = cfg.formats[0]
+    f = H.Fmt(we, wf, 0)
+    n = 2
+    x, w = inputs.draw(cfg, n=n)
+    if cfg.dw:
+        y = gpu_conv_dw(x, w, f, cfg.stride, cfg.pad, 0)
+    else:
+        y = gpu_conv(x, w, f, stride=cfg.stride, pad=cfg.pad, prepared=True)
+    xq, wq = oracle.encode_f32(x, we, wf), oracle.encode_f32(w, we, wf)
+    if cfg.dw:
+        exp = oracle.conv2d_dw(xq, wq, we, wf, wf + 1, 0, cfg.stride, cfg.pad, 0)
+        assert np.array_equal(y, exp)
+    else:
+        idx = np.random.default_rng(3).integers(0, y.size, 512)
+        exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wf + 1, 0, cfg.stride, cfg.pad, 0)
+        assert np.array_equal(y.ravel()[idx], exp)
