@@ -126,7 +126,11 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
  *
  * hobf_wtab_words: size in uint32 words of the table buffer for these weights,
  * or -1 if the format has no table kernel (wf > 10, extended class).
- * Layout: [kh][kw][cin][ceil(cout/32)][2^wf + 3 rows][roundup(wf + we + 6, 4) planes]. */
+ * Layout: [ceil(cout/32)][cin][kh][kw][2^wf + 3 rows][stride] uint32, where an
+ * entry has NPT = roundup(wfo + we + 5, 4) planes and rows are padded to
+ * stride = NPT if NPT/4 is odd, else NPT + 4 words (conflict-free 128-bit row
+ * gathers from shared memory); everything one 32-channel output group needs
+ * for one input channel is one contiguous block (one bulk copy). */
 int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t cout);
 
 /* Build the weight table from weight planes (layout as for hobf_conv2d). */
@@ -207,8 +211,12 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
  * per (pixel, 32-Cout group), kernel row of 3 taps unrolled, <= 56 registers;
  * 4 = table entry of the next tap prefetched (large tables); 5 = one-warp CTAs
  * with a 3-deep prefetch ring (fewer warps than SMSPs); 6 = three kernel rows
- * (one input channel) per unrolled loop body, <= 64 registers.  Variants 3
- * and 6 need kw == 3 (others fall back to the generic loop).  Every variant
+ * (one input channel) per unrolled loop body, <= 64 registers; 7 = the
+ * weight-table block of each input channel staged in shared memory by TMA bulk
+ * copies (double-buffered, mbarrier completion), 256-thread CTAs -- needs
+ * 2 * kh*kw * (2^wf + 3) * stride * 4 bytes <= 50 KB (wf <= 5 for 3x3), else it
+ * falls back to variant 6.  Variants 3 and 6 need kw == 3 (others fall back to
+ * the generic loop).  Every variant
  * runs the same circuit over the same serial (c, kh, kw) order: identical
  * results.  Unknown variants -> HOBF_EINVAL. */
 hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,

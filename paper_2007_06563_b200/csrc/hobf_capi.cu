@@ -303,12 +303,13 @@ __global__ void __launch_bounds__(256) quantize_acts_kernel(const float* __restr
 // its weight from the planes (shfl transpose), computes its entry, and the
 // entry bits are ballot-transposed back into NPT planes.
 __global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restrict__ wplanes, int64_t wrows, int G,
-                                                         int we, int wf, int wfo, int rnd,
+                                                         int cin, int khw, int we, int wf, int wfo, int rnd,
                                                          uint32_t* __restrict__ wtab) {
   const int lane = threadIdx.x & 31;
   const int npi = (3 + we + wf + 3) / 4 * 4;
   const int rows = tab_rows(wf);
   const int npt = (tab_width(we, wfo) + 3) / 4 * 4;
+  const int S = hobf::tab_stride(npt);
   // item = (weight row, group, chunk of 32 table rows): the weight is decoded once
   // per item and reused for the chunk's rows.
   const int chunks = (rows + 31) / 32;
@@ -337,8 +338,13 @@ __global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restr
         }
       }
 #pragma unroll
+      // weight row (tap, c) of group g -> table block [g][c][tap] (hobf_words.cuh);
+      // the stride padding words stay zero
+      const int64_t wrow = grp / G, g = grp % G;
+      const int64_t blk = (g * cin + wrow % cin) * khw + wrow / cin;
+#pragma unroll
       for (int u = 0; u < U; u++)
-        if (lane < npt && r + u < r1) wtab[(grp * rows + r + u) * npt + lane] = out[u];
+        if (lane < S && r + u < r1) wtab[(blk * rows + r + u) * S + lane] = lane < npt ? out[u] : 0u;
     }
   }
 }
@@ -558,6 +564,11 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
   return HOBF_OK;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 // Kernel variant of hobf_conv2d_prepared (see launch_conv_tab); HOBF_CONV_VARIANT overrides.
 static int conv_tab_variant() {
   static int v = -1;
@@ -577,7 +588,7 @@ int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t
   if (!fmt_ok(f.we, f.wf) || kh <= 0 || kw <= 0 || cin <= 0 || cout <= 0) return -1;
   if (!tab_format(f)) return -1;
   const int64_t npt = (tab_width(f.we, hobf_out_wf(f)) + 3) / 4 * 4;
-  return (int64_t)kh * kw * cin * ((cout + 31) / 32) * tab_rows(f.wf) * npt;
+  return (int64_t)kh * kw * cin * ((cout + 31) / 32) * tab_rows(f.wf) * hobf::tab_stride((int)npt);
 }
 
 hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cin,
@@ -591,8 +602,8 @@ hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t
   const int G = (cout + 31) / 32;
   const int64_t wrows = (int64_t)kh * kw * cin;
   const int64_t items = wrows * G * ((tab_rows(f.wf) + 31) / 32);
-  build_wtab_kernel<<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(d_w_planes, wrows, G, f.we, f.wf,
-                                                                          hobf_out_wf(f), f.round, d_wtab);
+  build_wtab_kernel<<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(d_w_planes, wrows, G, cin, kh * kw, f.we,
+                                                                          f.wf, hobf_out_wf(f), f.round, d_wtab);
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;
@@ -654,7 +665,7 @@ hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t 
                                     uint32_t* d_y_planes, int32_t variant, hobf_stream stream) {
   const uint32_t* d_x_planes = d_xrec;
   g_last_launches = 0;
-  if (variant != 0 && (variant < 3 || variant > 6)) return HOBF_EINVAL;
+  if (variant != 0 && (variant < 3 || variant > 7)) return HOBF_EINVAL;
   if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
     return HOBF_EINVAL;
   if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)
@@ -673,6 +684,7 @@ hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t 
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
   a.variant = variant;
+  a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
   if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;
   a.row_mul = 1u << 12;
   for (int j = 0; j < 32; j++) a.lift[j] = 1u << (31 - j);

@@ -16,6 +16,7 @@ struct ConvArgs {
                        // 1: y = planes of the next layer's F(we, next_wf) [pix][G][roundup(3+we+next_wf, 4)]
                        // 2: y = next layer's activation records, F(we, next_wf), [n][cout][ho+2np][wo+2np]
   int next_wf, next_pad;
+  int smem_cfg;        // variant 7 CTA shape override (development; 0 = auto)
   int one;             // always 1 (opaque to the compiler, see bcast_bit)
   unsigned two;        // always 2 (see bit01)
   unsigned row_mul;    // 2^12: IMAD.HI(rec, row_mul) = rec >> 20 (table row of an activation record)

@@ -273,7 +273,7 @@ struct TabTap {
     for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
     SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
     const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
-    const uint4* pt4 = reinterpret_cast<const uint4*>(tblock + (int64_t)row * F::NPT);
+    const uint4* pt4 = reinterpret_cast<const uint4*>(tblock + (int64_t)row * tab_stride(F::NPT));
 #pragma unroll
     for (int q = 0; q < F::NPT / 4; q++) {
       const uint4 v = __ldg(pt4 + q);
@@ -288,7 +288,6 @@ struct TabTap {
 // runs (latency-bound configs, large tables).
 template <class F, int NT, int MINB, bool KW3, int PD, int RU = 1>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
-  const int G = (a.cout + 31) >> 5;
   const int g = blockIdx.y;
   const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pix >= (int64_t)a.n * a.ho * a.wo) return;
@@ -305,11 +304,12 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   // record of (ni, c, oy*stride + kh, ox*stride + kw) = rbase[c*Hp*Wp + kh*Wp + kw]
   const uint32_t* __restrict__ rbase =
       a.x + ((int64_t)ni * a.cin * Hp + (int64_t)oy * a.stride) * Wp + (int64_t)ox * a.stride;
-  const int64_t tstride = (int64_t)G * F::TAB_ROWS * F::NPT;  // next (kh, kw, c) table block
-  const uint32_t* __restrict__ tbase = a.wt + (int64_t)g * F::TAB_ROWS * F::NPT;
+  // table block (c, kh, kw) of group g: [g][c][kh][kw] blocks of TAB_ROWS x stride words (hobf_words.cuh)
+  const int64_t tstride = (int64_t)F::TAB_ROWS * tab_stride(F::NPT);
+  const uint32_t* __restrict__ tbase = a.wt + (int64_t)g * a.cin * a.kh * KW * tstride;
   const int64_t cstride = (int64_t)Hp * Wp;
   auto rec_at = [&](int c, int kh, int kw) { return __ldg(rbase + c * cstride + kh * Wp + kw); };
-  auto tblock = [&](int c, int kh, int kw) { return tbase + ((int64_t)(kh * KW + kw) * a.cin + c) * tstride; };
+  auto tblock = [&](int c, int kh, int kw) { return tbase + ((int64_t)c * a.kh * KW + kh * KW + kw) * tstride; };
 
   if constexpr (PD == 0 && KW3) {
     // the 3 records of the next kernel row are loaded while this row's 3 MACs run
@@ -378,6 +378,170 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   store_out<F>(acc, a, pix, g, ni, oy, ox);
 }
 
+// ---------------------------------------------------------------------------
+// conv2d_prepared with the weight tables staged in shared memory.
+//
+// The per-thread table-row gathers are the part of the inner loop that costs
+// ALU issue efficiency when served by L1 (sector misses, wavefront
+// serialisation of 32 scattered 16-byte reads).  Here one CTA = one group of
+// 32 output channels x NT output pixels; for each input channel c the CTA's
+// whole table block [kh][kw][rows][stride] (hobf_words.cuh layout: one
+// contiguous block per (group, channel)) is brought into shared memory by one
+// TMA bulk copy (cp.async.bulk, completion on an mbarrier), double-buffered:
+// the copy of channel c+1 is in flight while channel c's kh*kw MACs run.  The
+// row stride makes a warp's 128-bit row gathers (nearly) bank-conflict-free.
+// Records stay in global memory (one coalesced 4-byte load per tap, the next
+// kernel row's records prefetched).  Same circuit, same serial (c, kh, kw)
+// order as conv_tab_kernel: identical results.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// TMA bulk copy global -> shared (this CTA), completing `bytes` on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+template <class F>
+constexpr int tab_block_words(int khw) {
+  return khw * F::TAB_ROWS * tab_stride(F::NPT);
+}
+
+// One tap of the staged-table MAC: broadcast planes of the record (FMA pipe),
+// the row gather from shared memory, the generated circuit.
+template <class F>
+__device__ __forceinline__ void smem_tap(uint32_t* acc, uint32_t rec, const uint32_t* __restrict__ tblk,
+                                         const ConvArgs& a) {
+  constexpr int S = tab_stride(F::NPT), WF = F::WF, WE = F::WE;
+  uint32_t EA[WE], SX[1], T[F::NPT];
+#pragma unroll
+  for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
+  SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
+  const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
+  const uint4* pt4 = reinterpret_cast<const uint4*>(tblk + (int)row * S);
+#pragma unroll
+  for (int q = 0; q < F::NPT / 4; q++) {
+    const uint4 v = pt4[q];
+    T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
+  }
+  F::mac_tab(acc, T, EA, SX);
+}
+
+// CC input channels per staged buffer (one TMA bulk copy of CC contiguous
+// channel blocks); K33: kh = kw = 3, the channel's nine taps fully unrolled.
+template <class F, int NT, int MINB, int CC, bool K33>
+__global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
+  extern __shared__ __align__(128) uint32_t smem_tab[];  // [2][CC][kh*kw][rows][stride]
+  __shared__ __align__(8) uint64_t full[2];
+  constexpr int S = tab_stride(F::NPT), R = F::TAB_ROWS;
+  const int g = blockIdx.y;
+  const int64_t npix = (int64_t)a.n * a.ho * a.wo;
+  const int64_t pix_raw = (int64_t)blockIdx.x * NT + threadIdx.x;
+  const bool valid = pix_raw < npix;
+  const int64_t pix = valid ? pix_raw : npix - 1;  // idle threads still join the CTA barriers
+  const int ox = (int)(pix % a.wo);
+  const int oy = (int)((pix / a.wo) % a.ho);
+  const int ni = (int)(pix / ((int64_t)a.wo * a.ho));
+  const int Hp = a.h + 2 * a.pad, Wp = a.w + 2 * a.pad;
+  const int KH = K33 ? 3 : a.kh, KW = K33 ? 3 : a.kw, KHW = KH * KW;
+  const uint32_t blk = (uint32_t)(KHW * R * S);  // words per (group, channel) block
+  const uint32_t* __restrict__ gsrc = a.wt + (int64_t)g * a.cin * blk;
+  const int nchunks = (a.cin + CC - 1) / CC;
+
+  uint32_t acc[F::NOUT];
+#pragma unroll
+  for (int j = 0; j < F::NOUT; j++) acc[j] = 0u;  // +0 (L9)
+
+  const uint32_t* __restrict__ rbase =
+      a.x + ((int64_t)ni * a.cin * Hp + (int64_t)oy * a.stride) * Wp + (int64_t)ox * a.stride;
+  const int64_t cstride = (int64_t)Hp * Wp;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int k) {  // chunk k -> buffer k & 1
+    const int c0 = k * CC, cc = min(CC, a.cin - c0);
+    const uint32_t bytes = (uint32_t)cc * blk * 4u;
+    mbar_expect_tx(&full[k & 1], bytes);
+    bulk_g2s(smem_tab + (k & 1) * CC * blk, gsrc + (int64_t)c0 * blk, bytes, &full[k & 1]);
+  };
+  if (threadIdx.x == 0) issue(0);
+  uint32_t rn[3];  // K33: records of the next kernel row
+  if (K33) {
+#pragma unroll
+    for (int kw = 0; kw < 3; kw++) rn[kw] = __ldg(rbase + kw);
+  }
+#pragma unroll 1
+  for (int k = 0; k < nchunks; k++) {
+    if (threadIdx.x == 0 && k + 1 < nchunks) {
+      // buffer (k+1)&1 was last read in chunk k-1, which ended with a CTA barrier
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + 1);
+    }
+    mbar_wait(&full[k & 1], (uint32_t)(k >> 1) & 1u);
+    const uint32_t* __restrict__ tbuf = smem_tab + (k & 1) * CC * blk;
+    const int c0 = k * CC, cc = min(CC, a.cin - c0);
+#pragma unroll 1
+    for (int ci = 0; ci < cc; ci++) {
+      const int c = c0 + ci;
+      const uint32_t* __restrict__ tb = tbuf + ci * blk;
+      const uint32_t* __restrict__ rc_base = rbase + c * cstride;
+      if (K33) {
+#pragma unroll
+        for (int kh = 0; kh < 3; kh++) {
+          uint32_t rc[3];
+#pragma unroll
+          for (int kw = 0; kw < 3; kw++) rc[kw] = rn[kw];
+          // next kernel row: same channel, or the next channel's first row
+          if (kh < 2 || c + 1 < a.cin) {
+            const uint32_t* nrow = kh < 2 ? rc_base + (kh + 1) * Wp : rc_base + cstride;
+#pragma unroll
+            for (int kw = 0; kw < 3; kw++) rn[kw] = __ldg(nrow + kw);
+          }
+#pragma unroll
+          for (int kw = 0; kw < 3; kw++) smem_tap<F>(acc, rc[kw], tb + (kh * 3 + kw) * R * S, a);
+        }
+      } else {
+#pragma unroll 1
+        for (int kh = 0; kh < KH; kh++) {
+#pragma unroll 1
+          for (int kw = 0; kw < KW; kw++)
+            smem_tap<F>(acc, __ldg(rc_base + kh * Wp + kw), tb + (kh * KW + kw) * R * S, a);
+        }
+      }
+    }
+    __syncthreads();  // buffer k&1 is refilled at chunk k+2's issue (iteration k+1)
+  }
+  if (!valid) return;
+  F::canon(acc, acc);  // the chain keeps a relaxed accumulator (fpgen.build_mac_tab)
+  if (a.relu) F::relu(acc, acc);
+  store_out<F>(acc, a, pix, g, ni, oy, ox);
+}
+
 // mac_planes: acc[i] = add(acc[i], mul(a[i], b[i])) lane-wise on plane groups.
 template <class F>
 __global__ void __launch_bounds__(256) mac_planes_kernel(uint32_t* __restrict__ acc_p, const uint32_t* __restrict__ a_p,
@@ -412,14 +576,44 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const bool k3 = a.kw == 3;
   int variant = a.variant;
   const int64_t warps = (npix + 31) / 32 * gy;
+  // shared-memory table staging (variant 7): CTAs of NT7 threads, buffers of CC7
+  // channel blocks, double-buffered, within the shared memory of 4 (or 8) CTAs / SM
+  const int64_t blk_bytes = (int64_t)tab_block_words<F>(a.kh * a.kw) * 4;
+  const bool k33 = k3 && a.kh == 3;
+  const bool smem_ok = 2 * blk_bytes <= 50 * 1024;
   if (variant == 0) {
-    // auto: with fewer warps than SMSPs the reduction chains are latency-bound:
-    // one-warp CTAs (so every SM gets work) running the software-pipelined
-    // kernel; the pipelined kernel also when the table rows do not stay L1
-    // resident (wF >= 8) or there are < ~4 warps per SMSP to hide load latency;
-    // otherwise the KW=3 kernel with three kernel rows per unrolled loop body
-    // (more independent work in view of the scheduler) at <= 64 registers.
-    variant = warps < 148 * 4 * 2 ? 5 : (F::WF >= 8 ? 4 : (k3 ? 6 : 3));
+    // auto: with fewer warps than 2 per SMSP the reduction chains are latency-bound:
+    // one-warp CTAs (so every SM gets work) running the software-pipelined kernel;
+    // otherwise the tables staged in shared memory when a channel block pair fits
+    // (wF <= 5 for 3x3), else the L1-served kernels: prefetching one tap ahead when
+    // the table rows do not stay L1 resident (wF >= 8), or three kernel rows per
+    // unrolled loop body at <= 64 registers.
+    variant = warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : (F::WF >= 8 ? 4 : (k3 ? 6 : 3));
+  }
+  if (variant == 7 && !smem_ok) variant = 6;
+  if (variant == 7) {
+    const int sm = a.smem_cfg;  // development override (HOBF_SMEM_CFG): 0 auto, 1..4
+    // >= 8 warps per SMSP of work: 128-thread CTAs x 8 per SM (one channel block per
+    // buffer) when 8 x 2 blocks fit the SM's shared memory; otherwise (fewer warps, or
+    // larger blocks) 256-thread CTAs x 4 per SM (measured on C3 / C4 / C5)
+    const int cfg = sm ? sm : ((warps >= 148 * 4 * 8 && 16 * blk_bytes <= 216 * 1024) ? 2 : 3);
+    auto go = [&](auto kern, int nt, int cc) {
+      static bool attr = false;  // once per kernel instantiation: allow up to 200 KB of dynamic smem
+      if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      kern<<<grid(nt), nt, (size_t)(2 * cc * blk_bytes), s>>>(a);
+    };
+    if (k33) {
+      if (cfg == 1) go(conv_tab_smem_kernel<F, 128, 8, 2, true>, 128, 2);
+      else if (cfg == 2) go(conv_tab_smem_kernel<F, 128, 8, 1, true>, 128, 1);
+      else if (cfg == 3) go(conv_tab_smem_kernel<F, 256, 4, 1, true>, 256, 1);
+      else go(conv_tab_smem_kernel<F, 256, 4, 2, true>, 256, 2);
+    } else {
+      go(conv_tab_smem_kernel<F, 256, 4, 1, false>, 256, 1);
+    }
+    return cudaGetLastError();
   }
   if (variant == 6 && k3) {  // KW=3, 3 kernel rows (one input channel) per unrolled body, <= 64 registers
     conv_tab_kernel<F, 128, 8, true, 0, 3><<<grid(128), 128, 0, s>>>(a);

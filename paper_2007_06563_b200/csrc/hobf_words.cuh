@@ -47,4 +47,14 @@ __device__ __forceinline__ uint32_t requant_word(uint32_t x, int we, int wfi, in
   return (1u << top) | (s << (wfo + we)) | (e << wfo) | f;
 }
 
+// Weight-table geometry (hobf_prepare_weights, hobf_conv2d_prepared).
+// Entry planes NPT = roundup(wfo + (we + 2) + 3, 4); rows are stored with a
+// stride of tab_stride(NPT) words, chosen so that stride / 4 is odd: the 16-byte
+// segments of 8 consecutive rows then fall in 8 distinct shared-memory bank
+// quads, and a warp's 128-bit row gathers from a staged table are (nearly)
+// conflict-free.  Layout [ceil(cout/32)][cin][kh][kw][2^wF + 3 rows][stride]:
+// everything one output-channel group needs for one input channel is one
+// contiguous block (one bulk copy).
+__host__ __device__ constexpr int tab_stride(int npt) { return ((npt / 4) & 1) ? npt : npt + 4; }
+
 }  // namespace hobf

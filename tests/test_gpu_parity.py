@@ -246,7 +246,7 @@ def test_conv_prepared_full_vs_oracle(we, wf):
             assert np.array_equal(got, gpu_conv(x, w, f, relu=relu, prepared=False))
 
 
-@pytest.mark.parametrize("variant", [3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [3, 4, 5, 6, 7])
 @pytest.mark.parametrize("we,wf,kh,kw", [(5, 3, 3, 3), (4, 6, 2, 3), (5, 10, 3, 3), (6, 2, 3, 2)])
 def test_conv_prepared_every_schedule(variant, we, wf, kh, kw):
     """Every kernel schedule of hobf_conv2d_prepared_variant gives the oracle's words:

@@ -32,11 +32,12 @@ wp = H.quantize_pack(we, wf, torch.from_numpy(w.reshape(-1, cfg.cout)).cuda(), f
 g = H.gate_count(f)
 if a.kernel == "tables":
     wt = H.prepare_weights(f, wp, 3, 3, cfg.cin, cfg.cout)
-    xr = H.prepare_activations(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, 1)
-    run = lambda: H.conv2d_prepared(f, xr, cfg.n, cfg.h, cfg.w, cfg.cin, wt, 3, 3, cfg.cout)  # noqa: E731
+    xr = H.prepare_activations(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, cfg.pad)
+    run = lambda: H.conv2d_prepared(f, xr, cfg.n, cfg.h, cfg.w, cfg.cin, wt, 3, 3, cfg.cout,  # noqa: E731
+                                    cfg.stride, cfg.pad)
     G = g["mac_tab"]
 else:
-    run = lambda: H.conv2d(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, wp, 3, 3, cfg.cout)  # noqa: E731
+    run = lambda: H.conv2d(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, wp, 3, 3, cfg.cout, cfg.stride, cfg.pad)  # noqa: E731
     G = g["mac"]
 y0 = run()
 for _ in range(3):

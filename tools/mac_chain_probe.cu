@@ -15,6 +15,13 @@ using F = hobf_gen::F_e5m3_rne;
 // 2: + table entry gathered from an L1-resident table every MAC (like the conv).
 template <int NG, int MINB, int MODE>
 __global__ void __launch_bounds__(128, MINB) chain(uint32_t* out, const uint32_t* in, int iters, uint32_t m) {
+  const uint32_t m1 = m >> 24;  // 1 at run time (m = 0x01000193), opaque to the compiler
+  __shared__ __align__(16) uint32_t stab[16 * 20];  // MODE 4/5: 16 table rows, 20-word (80 B) or 16-word stride
+  if (MODE >= 4) {
+    for (int i = threadIdx.x; i < 16 * 20; i += blockDim.x) stab[i] = in[i];
+    __syncthreads();
+  }
+  const int32_t one = (int32_t)m1;
   uint32_t acc[NG][F::NOUT], T[F::NPT], EA[F::WE], SX[1];
   const uint32_t* p = in + (threadIdx.x & 31) * 64;
 #pragma unroll
@@ -29,12 +36,34 @@ __global__ void __launch_bounds__(128, MINB) chain(uint32_t* out, const uint32_t
   for (int it = 0; it < iters; it++) {
 #pragma unroll
     for (int i = 0; i < NG; i++) F::mac_tab(acc[i], T, EA, SX);
-    if (MODE >= 1) {
+    if (MODE == 1 || MODE == 2 || MODE >= 4) {
 #pragma unroll
       for (int j = 0; j < F::WE; j++) EA[j] = EA[j] * m + 0x7F4A7C15u;
       SX[0] = SX[0] * m + 1u;
     }
-    if (MODE == 2) {
+    if (MODE == 3) {
+      // like the conv: a per-tap record (L1-resident) -> exponent / sign planes by
+      // IMAD + IMAD.HI broadcasts, table row by IMAD.HI, then the row gather
+      const uint32_t rec = __ldg(in + 4096 + ((it * 37 + threadIdx.x) & 1023));
+#pragma unroll
+      for (int j = 0; j < F::WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * (1u << (31 - F::WF - j)) * m1), one);
+      SX[0] = (uint32_t)__mulhi((int32_t)(rec * (1u << (31 - F::WF - F::WE)) * m1), one);
+      const uint32_t row = __umulhi(rec, 16u * m1);
+      const uint4* q = reinterpret_cast<const uint4*>(in + row * 64);
+#pragma unroll
+      for (int j = 0; j < F::NPT / 4; j++) {
+        const uint4 v = __ldg(q + j);
+        T[4 * j] = v.x; T[4 * j + 1] = v.y; T[4 * j + 2] = v.z; T[4 * j + 3] = v.w;
+      }
+    } else if (MODE == 4 || MODE == 5) {
+      const uint32_t r = (EA[0] * m) >> 28;
+      const uint4* q = reinterpret_cast<const uint4*>(stab + r * (MODE == 4 ? 20 : 16));
+#pragma unroll
+      for (int j = 0; j < F::NPT / 4; j++) {
+        const uint4 v = q[j];
+        T[4 * j] = v.x; T[4 * j + 1] = v.y; T[4 * j + 2] = v.z; T[4 * j + 3] = v.w;
+      }
+    } else if (MODE == 2) {
       const uint4* q = reinterpret_cast<const uint4*>(in + ((EA[0] * m) >> 28) * 64);  // row from the "activation"
 #pragma unroll
       for (int j = 0; j < F::NPT / 4; j++) {
@@ -73,13 +102,15 @@ void run(int blocks, int iters, uint32_t* d, uint32_t* din) {
 int main() {
   uint32_t *d, *din;
   cudaMalloc(&d, 148 * 64 * 128 * 4);
-  cudaMalloc(&din, 32 * 64 * 4 * 16);
-  static uint32_t h[32 * 64 * 16];
-  for (int i = 0; i < 32 * 64 * 16; i++) h[i] = 0x9E3779B9u * (i + 1);
+  cudaMalloc(&din, 32 * 64 * 4 * 16 + 4096 * 4);
+  static uint32_t h[32 * 64 * 16 + 1024];
+  for (int i = 0; i < 32 * 64 * 16 + 1024; i++) h[i] = 0x9E3779B9u * (i + 1);
   cudaMemcpy(din, h, sizeof(h), cudaMemcpyHostToDevice);
   for (int b : {148, 296, 592, 1332}) run<1, 9, 0>(b, 2000, d, din);
   for (int b : {148, 296, 592, 1332}) run<1, 9, 1>(b, 2000, d, din);
   for (int b : {148, 296, 592, 1332}) run<1, 9, 2>(b, 2000, d, din);
-  for (int b : {148, 296, 592}) run<2, 4, 2>(b, 1000, d, din);
+  for (int b : {148, 296, 592, 1184}) run<1, 8, 3>(b, 2000, d, din);
+  for (int b : {148, 296, 592, 1184}) run<1, 8, 4>(b, 2000, d, din);
+  for (int b : {148, 296, 592, 1184}) run<1, 8, 5>(b, 2000, d, din);
   return 0;
 }
