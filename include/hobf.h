@@ -128,8 +128,8 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
  * or -1 if the format has no table kernel (wf > 10, extended class).
  * Layout: [ceil(cout/32)][cin][kh][kw][2^wf + 3 rows][stride] uint32, where an
  * entry has NPT = roundup(wfo + we + 5, 4) planes and rows are padded to
- * stride = NPT if NPT/4 is odd, else NPT + 4 words (conflict-free 128-bit row
- * gathers from shared memory); everything one 32-channel output group needs
+ * stride = NPT + 4 words when wf <= 5 and NPT/4 is even (conflict-free 128-bit
+ * row gathers from shared memory), else stride = NPT; everything one 32-channel output group needs
  * for one input channel is one contiguous block (one bulk copy). */
 int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t cout);
 

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restr
   const int npi = (3 + we + wf + 3) / 4 * 4;
   const int rows = tab_rows(wf);
   const int npt = (tab_width(we, wfo) + 3) / 4 * 4;
-  const int S = hobf::tab_stride(npt);
+  const int S = hobf::tab_stride(npt, wf);
   // item = (weight row, group, chunk of 32 table rows): the weight is decoded once
   // per item and reused for the chunk's rows.
   const int chunks = (rows + 31) / 32;
@@ -588,7 +588,7 @@ int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t
   if (!fmt_ok(f.we, f.wf) || kh <= 0 || kw <= 0 || cin <= 0 || cout <= 0) return -1;
   if (!tab_format(f)) return -1;
   const int64_t npt = (tab_width(f.we, hobf_out_wf(f)) + 3) / 4 * 4;
-  return (int64_t)kh * kw * cin * ((cout + 31) / 32) * tab_rows(f.wf) * hobf::tab_stride((int)npt);
+  return (int64_t)kh * kw * cin * ((cout + 31) / 32) * tab_rows(f.wf) * hobf::tab_stride((int)npt, f.wf);
 }
 
 hobf_status hobf_prepare_weights(hobf_fmt f, const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cin,

@@ -273,7 +273,7 @@ struct TabTap {
     for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
     SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
     const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
-    const uint4* pt4 = reinterpret_cast<const uint4*>(tblock + (int64_t)row * tab_stride(F::NPT));
+    const uint4* pt4 = reinterpret_cast<const uint4*>(tblock + (int64_t)row * tab_stride(F::NPT, F::WF));
 #pragma unroll
     for (int q = 0; q < F::NPT / 4; q++) {
       const uint4 v = __ldg(pt4 + q);
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   const uint32_t* __restrict__ rbase =
       a.x + ((int64_t)ni * a.cin * Hp + (int64_t)oy * a.stride) * Wp + (int64_t)ox * a.stride;
   // table block (c, kh, kw) of group g: [g][c][kh][kw] blocks of TAB_ROWS x stride words (hobf_words.cuh)
-  const int64_t tstride = (int64_t)F::TAB_ROWS * tab_stride(F::NPT);
+  const int64_t tstride = (int64_t)F::TAB_ROWS * tab_stride(F::NPT, F::WF);
   const uint32_t* __restrict__ tbase = a.wt + (int64_t)g * a.cin * a.kh * KW * tstride;
   const int64_t cstride = (int64_t)Hp * Wp;
   auto rec_at = [&](int c, int kh, int kw) { return __ldg(rbase + c * cstride + kh * Wp + kw); };
@@ -425,7 +425,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 template <class F>
 constexpr int tab_block_words(int khw) {
-  return khw * F::TAB_ROWS * tab_stride(F::NPT);
+  return khw * F::TAB_ROWS * tab_stride(F::NPT, F::WF);
 }
 
 // One tap of the staged-table MAC: broadcast planes of the record (FMA pipe),
@@ -433,7 +433,7 @@ constexpr int tab_block_words(int khw) {
 template <class F>
 __device__ __forceinline__ void smem_tap(uint32_t* acc, uint32_t rec, const uint32_t* __restrict__ tblk,
                                          const ConvArgs& a) {
-  constexpr int S = tab_stride(F::NPT), WF = F::WF, WE = F::WE;
+  constexpr int S = tab_stride(F::NPT, F::WF), WF = F::WF, WE = F::WE;
   uint32_t EA[WE], SX[1], T[F::NPT];
 #pragma unroll
   for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
@@ -454,7 +454,7 @@ template <class F, int NT, int MINB, int CC, bool K33>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
   extern __shared__ __align__(128) uint32_t smem_tab[];  // [2][CC][kh*kw][rows][stride]
   __shared__ __align__(8) uint64_t full[2];
-  constexpr int S = tab_stride(F::NPT), R = F::TAB_ROWS;
+  constexpr int S = tab_stride(F::NPT, F::WF), R = F::TAB_ROWS;
   const int g = blockIdx.y;
   const int64_t npix = (int64_t)a.n * a.ho * a.wo;
   const int64_t pix_raw = (int64_t)blockIdx.x * NT + threadIdx.x;

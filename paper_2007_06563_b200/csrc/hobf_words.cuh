@@ -49,12 +49,16 @@ __device__ __forceinline__ uint32_t requant_word(uint32_t x, int we, int wfi, in
 
 // Weight-table geometry (hobf_prepare_weights, hobf_conv2d_prepared).
 // Entry planes NPT = roundup(wfo + (we + 2) + 3, 4); rows are stored with a
-// stride of tab_stride(NPT) words, chosen so that stride / 4 is odd: the 16-byte
-// segments of 8 consecutive rows then fall in 8 distinct shared-memory bank
-// quads, and a warp's 128-bit row gathers from a staged table are (nearly)
-// conflict-free.  Layout [ceil(cout/32)][cin][kh][kw][2^wF + 3 rows][stride]:
+// stride of tab_stride(NPT, wf) words.  For the formats whose tables are staged
+// in shared memory (wF <= 5) the stride is chosen so that stride / 4 is odd: the
+// 16-byte segments of 8 consecutive rows then fall in 8 distinct bank quads,
+// and a warp's 128-bit row gathers are (nearly) conflict-free.  Wider formats
+// are served from L1/L2 and keep stride = NPT (their 2^wF + 3 rows make the
+// tables large: C2's e5m10 tables must stay L2-resident).  Layout [ceil(cout/32)][cin][kh][kw][2^wF + 3 rows][stride]:
 // everything one output-channel group needs for one input channel is one
 // contiguous block (one bulk copy).
-__host__ __device__ constexpr int tab_stride(int npt) { return ((npt / 4) & 1) ? npt : npt + 4; }
+__host__ __device__ constexpr int tab_stride(int npt, int wf) {
+  return (wf > 5 || ((npt / 4) & 1)) ? npt : npt + 4;
+}
 
 }  // namespace hobf
