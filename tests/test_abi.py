@@ -66,6 +66,18 @@ def test_argument_errors_are_synchronous_and_need_no_gpu():
     assert lib.hobf_conv2d(f, None, 1, 4, 4, 4, None, 3, 3, 4, 0, 1, 0, None, None) == 1
     assert lib.hobf_mac_planes(f, None, None, None, 5, None) == 1
     assert lib.hobf_status_str(3) == b"unsupported format (no generated kernel)"
+    # chaining epilogue / schedule validation happens before any launch: fake (never
+    # dereferenced) 16-byte-aligned pointers reach the checks without a GPU
+    P = 1 << 20
+    E = hobf.hobf_epilogue
+    bad = [E(hobf.OUT_NEXT_RECORDS, 0, 1), E(hobf.OUT_NEXT_RECORDS, 3, -1), E(hobf.OUT_NEXT_RECORDS, 12, 1),
+           E(hobf.OUT_NEXT_PLANES, 30, 0), E(7, 3, 1)]
+    for ep in bad:
+        assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, ep, P, 0, None) == 1
+        assert lib.hobf_conv2d_dw(f, P, 1, 4, 4, 8, P, 3, 3, 1, 1, 0, ep, P, None) == 1
+    assert lib.hobf_conv2d_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(hobf.OUT_NEXT_RECORDS, 3, 1), P, None) == 1
+    assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(0, 0, 0), P, 9, None) == 1
+    assert lib.hobf_conv2d_dw(f, P, 1, 2, 2, 8, P, 5, 5, 1, 0, 0, E(0, 0, 0), P, None) == 2
 
 
 def test_binding_fails_loudly_without_library(tmp_path):

@@ -41,7 +41,34 @@ __global__ void __launch_bounds__(128, MINB) chain(uint32_t* out, const uint32_t
       for (int j = 0; j < F::WE; j++) EA[j] = EA[j] * m + 0x7F4A7C15u;
       SX[0] = SX[0] * m + 1u;
     }
-    if (MODE == 3) {
+    if (MODE == 7) {
+      // pre-broadcast records: 8 words per activation (EA planes, SX plane, row),
+      // coalesced 2 x 128-bit loads per tap; table row gathered from shared memory
+      const uint4* pr = reinterpret_cast<const uint4*>(in + 4096) + 2 * ((it * 37 + threadIdx.x) & 511);
+      const uint4 r0 = __ldg(pr), r1 = __ldg(pr + 1);
+      EA[0] = r0.x; EA[1] = r0.y; EA[2] = r0.z; EA[3] = r0.w; EA[4] = r1.x; SX[0] = r1.y;
+      const uint32_t row = r1.z & 15u;
+      const uint4* q = reinterpret_cast<const uint4*>(stab + row * 20);
+#pragma unroll
+      for (int j = 0; j < F::NPT / 4; j++) {
+        const uint4 v = q[j];
+        T[4 * j] = v.x; T[4 * j + 1] = v.y; T[4 * j + 2] = v.z; T[4 * j + 3] = v.w;
+      }
+    } else if (MODE == 6) {
+      // the conv's per-tap work with the table in shared memory: record load,
+      // IMAD/IMAD.HI broadcasts, row by IMAD.HI, 80-byte-stride row gather
+      const uint32_t rec = __ldg(in + 4096 + ((it * 37 + threadIdx.x) & 1023));
+#pragma unroll
+      for (int j = 0; j < F::WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * (1u << (31 - F::WF - j)) * m1), one);
+      SX[0] = (uint32_t)__mulhi((int32_t)(rec * (1u << (31 - F::WF - F::WE)) * m1), one);
+      const uint32_t row = __umulhi(rec, 16u * m1);
+      const uint4* q = reinterpret_cast<const uint4*>(stab + row * 20);
+#pragma unroll
+      for (int j = 0; j < F::NPT / 4; j++) {
+        const uint4 v = q[j];
+        T[4 * j] = v.x; T[4 * j + 1] = v.y; T[4 * j + 2] = v.z; T[4 * j + 3] = v.w;
+      }
+    } else if (MODE == 3) {
       // like the conv: a per-tap record (L1-resident) -> exponent / sign planes by
       // IMAD + IMAD.HI broadcasts, table row by IMAD.HI, then the row gather
       const uint32_t rec = __ldg(in + 4096 + ((it * 37 + threadIdx.x) & 1023));
@@ -106,11 +133,9 @@ int main() {
   static uint32_t h[32 * 64 * 16 + 1024];
   for (int i = 0; i < 32 * 64 * 16 + 1024; i++) h[i] = 0x9E3779B9u * (i + 1);
   cudaMemcpy(din, h, sizeof(h), cudaMemcpyHostToDevice);
-  for (int b : {148, 296, 592, 1332}) run<1, 9, 0>(b, 2000, d, din);
-  for (int b : {148, 296, 592, 1332}) run<1, 9, 1>(b, 2000, d, din);
-  for (int b : {148, 296, 592, 1332}) run<1, 9, 2>(b, 2000, d, din);
-  for (int b : {148, 296, 592, 1184}) run<1, 8, 3>(b, 2000, d, din);
+  for (int b : {148, 1332}) run<1, 9, 1>(b, 2000, d, din);
   for (int b : {148, 296, 592, 1184}) run<1, 8, 4>(b, 2000, d, din);
-  for (int b : {148, 296, 592, 1184}) run<1, 8, 5>(b, 2000, d, din);
+  for (int b : {148, 296, 592, 1184}) run<1, 8, 6>(b, 2000, d, din);
+  for (int b : {148, 296, 592, 1184}) run<1, 8, 7>(b, 2000, d, din);
   return 0;
 }
