@@ -362,6 +362,9 @@ class Conv2d:
     def __init__(self, weight_f32: torch.Tensor, f: Fmt, stride: int = 1, pad: int = 1, relu: bool = False,
                  use_tables: bool = True):
         kh, kw, cin, cout = weight_f32.shape
+        if not weight_f32.is_cuda:  # marshalling: the library works on device memory
+            weight_f32 = weight_f32.to("cuda")
+        weight_f32 = weight_f32.to(torch.float32)
         self.f, self.kh, self.kw, self.cin, self.cout = f, kh, kw, cin, cout
         self.stride, self.pad, self.relu = stride, pad, relu
         self.w_planes = quantize_pack(f.we, f.wf, weight_f32.reshape(kh * kw * cin, cout).contiguous(), f.round)
@@ -380,6 +383,9 @@ class Conv2d:
     def __call__(self, x_f32: torch.Tensor) -> torch.Tensor:
         n, h, w, cin = x_f32.shape
         assert cin == self.cin
+        if not x_f32.is_cuda:
+            x_f32 = x_f32.to(self.w_planes.device)
+        x_f32 = x_f32.to(torch.float32)
         if self.wtab is not None:
             xrec = quantize_activations(self.f, x_f32.contiguous(), self.pad)
             yp = conv2d_prepared(self.f, xrec, n, h, w, cin, self.wtab, self.kh, self.kw, self.cout, self.stride,
