@@ -8,6 +8,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "../../include/hobf.h"
 #include "hobf_internal.h"
 #include "hobf_words.cuh"
@@ -58,44 +60,64 @@ __device__ __forceinline__ uint32_t canon_word(uint32_t v, int we, int wf) {
 // rounded at its own binade (RNE ties-to-even or RTZ), then overflow -> inf,
 // underflow (biased exponent < 0) -> zero keeping the sign (L5/L6).
 __device__ __forceinline__ uint32_t encode_f32(float f, int we, int wf, int rnd) {
+  // Branch-free (activations mix zeros, normals and the odd special within a
+  // warp): the finite nonzero path is always computed and the special classes
+  // are selected over it.
   const uint32_t u = __float_as_uint(f);
   const uint32_t sign = u >> 31;
   const int ex = (int)((u >> 23) & 0xFFu);
   const uint32_t man = u & 0x7FFFFFu;
   const int top = wf + we + 1;
-  if (ex == 0xFF) return man ? (3u << top) : ((2u << top) | (sign << (wf + we)));
-  if (ex == 0 && man == 0) return sign << (wf + we);
-  uint32_t M;
-  int e;
-  if (ex == 0) { M = man; e = -149; } else { M = man | 0x800000u; e = ex - 150; }
-  const int k = 31 - __clz(M);  // M = 1.xxx * 2^k
-  const int sh = k - wf;
-  uint32_t q;
-  if (sh <= 0) {
-    q = M << (-sh);
-  } else {
-    q = M >> sh;
-    const uint32_t rem = M & ((1u << sh) - 1u);
-    const uint32_t half = 1u << (sh - 1);
-    if (rnd == 0 && (rem > half || (rem == half && (q & 1u)))) q += 1u;
-  }
+  const uint32_t sfield = sign << (wf + we);
+  const uint32_t M = ex ? (man | 0x800000u) : man;  // exact value M * 2^e
+  const int e = ex ? ex - 150 : -149;
+  const int k = 31 - __clz(M | 1u);                  // M = 1.xxx * 2^k (M = 0 is selected away below)
+  const int sh = k - wf;                             // bits below the kept fraction
+  const int shr = sh > 0 ? sh : 0;
+  const uint32_t qd = M >> shr;
+  const uint32_t rem = M & ((1u << shr) - 1u);
+  const uint32_t half = sh > 0 ? 1u << (sh - 1) : 0u;
+  const bool up = rnd == 0 && sh > 0 && (rem > half || (rem == half && (qd & 1u)));
+  uint32_t q = sh > 0 ? qd + (up ? 1u : 0u) : (M << (-sh));
   int E = e + k + ((1 << (we - 1)) - 1);
-  if (q == (2u << wf)) { q >>= 1; E += 1; }
-  if (E > (1 << we) - 1) return (2u << top) | (sign << (wf + we));
-  if (E < 0) return sign << (wf + we);
-  return (1u << top) | (sign << (wf + we)) | ((uint32_t)E << wf) | (q - (1u << wf));
+  const bool carry = q == (2u << wf);
+  q = carry ? q >> 1 : q;
+  E += carry ? 1 : 0;
+  const uint32_t inf = (2u << top) | sfield;
+  const uint32_t normal = (1u << top) | sfield | ((uint32_t)E << wf) | (q - (1u << wf));
+  const uint32_t finite = E > (1 << we) - 1 ? inf : (E < 0 ? sfield : normal);
+  const uint32_t nonfinite = man ? (3u << top) : inf;
+  return ex == 0xFF ? nonfinite : ((ex == 0 && man == 0) ? sfield : finite);
 }
 
-// F(we, wf) word -> float32 (exact for we <= 7, wf <= 23).
+// F(we, wf) word -> float32 (exact for we <= 7, wf <= 23).  Branch-free: the
+// four exception classes are selected, not branched on (no divergence).
 __device__ __forceinline__ float decode_f32(uint32_t v, int we, int wf) {
   const uint32_t exc = (v >> (wf + we + 1)) & 3u;
-  const uint32_t sign = (v >> (wf + we)) & 1u;
-  if (exc == 0u) return __uint_as_float(sign << 31);
-  if (exc == 2u) return __uint_as_float((sign << 31) | 0x7F800000u);
-  if (exc == 3u) return __uint_as_float(0x7FC00000u);
+  const uint32_t sbit = ((v >> (wf + we)) & 1u) << 31;
   const int E = (int)((v >> wf) & ((1u << we) - 1u)) - ((1 << (we - 1)) - 1);
   const uint32_t frac = v & ((1u << wf) - 1u);
-  return __uint_as_float((sign << 31) | ((uint32_t)(E + 127) << 23) | (frac << (23 - wf)));
+  const uint32_t normal = sbit | ((uint32_t)(E + 127) << 23) | (frac << (23 - wf));
+  const uint32_t special = exc == 3u ? 0x7FC00000u : (sbit | (exc == 2u ? 0x7F800000u : 0u));
+  return __uint_as_float(exc == 1u ? normal : special);
+}
+
+// 32 x 32 bit-matrix transpose in registers (bit j of A[i] <-> bit i of A[j]):
+// five rounds of block swaps, the s x s off-diagonal blocks of every 2s x 2s
+// block exchanged with one shift and two xors per row pair.
+__device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u
+                                                                                                   : 0x55555555u;
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      if (i & s) continue;
+      const uint32_t t = ((A[i] >> s) ^ A[i + s]) & m;
+      A[i + s] ^= t;
+      A[i] ^= t << s;
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------- pack / unpack
@@ -110,15 +132,24 @@ __global__ void __launch_bounds__(256) pack_kernel(const void* __restrict__ src,
   const int64_t G = (C + 31) >> 5;
   const int64_t items = rows * G;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool dense = (C & 31) == 0;  // element (r, 32g + l) is then at it * 32 + l: no division
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
-    const int64_t r = it / G;
-    const int64_t c = (it - r * G) * 32 + lane;
+    int64_t idx;
+    bool ok = true;
+    if (dense) {
+      idx = it * 32 + lane;
+    } else {
+      const int64_t r = it / G;
+      const int64_t c = (it - r * G) * 32 + lane;
+      ok = c < C;
+      idx = r * C + c;
+    }
     uint32_t v = 0u;
-    if (c < C) {
+    if (ok) {
       if (FROM_F32)
-        v = encode_f32(__ldg(reinterpret_cast<const float*>(src) + r * C + c), we, wf, rnd);
+        v = encode_f32(__ldg(reinterpret_cast<const float*>(src) + idx), we, wf, rnd);
       else
-        v = canon_word(__ldg(reinterpret_cast<const uint32_t*>(src) + r * C + c), we, wf);
+        v = canon_word(__ldg(reinterpret_cast<const uint32_t*>(src) + idx), we, wf);
     }
     uint32_t mine = 0u;
     for (int j = 0; j < np; j++) {
@@ -137,6 +168,7 @@ __global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict_
   const int64_t items = rows * G;
   const int nb = 3 + we + wf;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool dense = (C & 31) == 0;  // element (r, 32g + l) is then at it * 32 + l: no division
   // UNR groups per warp iteration: their plane loads are all in flight before the
   // shuffles (the loop body is otherwise one dependent load -> shfl -> store chain).
   constexpr int UNR = 4;
@@ -149,19 +181,85 @@ __global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict_
       const int64_t it = it0 + u;
       if (it >= items) break;
       uint32_t v = 0u;
-      for (int j = 0; j < nb; j++) {
+      for (int j = nb - 1; j >= 0; j--) {  // bit j of v = bit `lane` of plane j
         const uint32_t pj = __shfl_sync(0xffffffffu, mine[u], j);
-        v |= ((pj >> lane) & 1u) << j;
+        v = (v << 1) | ((pj >> lane) & 1u);
       }
-      const int64_t r = it / G;
-      const int64_t c = (it - r * G) * 32 + lane;
-      if (c < C) {
+      int64_t idx;
+      bool ok = true;
+      if (dense) {
+        idx = it * 32 + lane;
+      } else {
+        const int64_t r = it / G;
+        const int64_t c = (it - r * G) * 32 + lane;
+        ok = c < C;
+        idx = r * C + c;
+      }
+      if (ok) {
         if (TO_F32)
-          reinterpret_cast<float*>(dst)[r * C + c] = decode_f32(v, we, wf);
+          reinterpret_cast<float*>(dst)[idx] = decode_f32(v, we, wf);
         else
-          reinterpret_cast<uint32_t*>(dst)[r * C + c] = v;
+          reinterpret_cast<uint32_t*>(dst)[idx] = v;
       }
     }
+  }
+}
+
+// Unpack, one thread per 32-lane group (the fast path): the group's NP plane
+// words arrive by 128-bit loads (consecutive threads = consecutive groups:
+// coalesced), a register transpose turns planes into the 32 lanes' words, and
+// the 32 outputs leave as eight 128-bit stores.  No shuffles, no division.
+// Used when C is a multiple of 32 (dense rows) and dst is 16-byte aligned.
+template <bool TO_F32, int NP>
+__global__ void __launch_bounds__(256) unpack_t_kernel(const uint32_t* __restrict__ planes, int64_t items, int we,
+                                                       int wf, void* __restrict__ dst) {
+  const int nb = 3 + we + wf;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t A[32];
+    const uint4* src = reinterpret_cast<const uint4*>(planes + it * NP);
+#pragma unroll
+    for (int q = 0; q < NP / 4; q++) {
+      const uint4 v = __ldg(src + q);
+      A[4 * q] = v.x; A[4 * q + 1] = v.y; A[4 * q + 2] = v.z; A[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int j = NP; j < 32; j++) A[j] = 0u;
+#pragma unroll
+    for (int j = 0; j < NP; j++)
+      if (j >= nb) A[j] = 0u;  // padding planes are zero anyway; keep the words exact
+    transpose32(A);
+    uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(dst) + it * 32);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      uint4 o;
+      if (TO_F32) {
+        o.x = __float_as_uint(decode_f32(A[4 * q], we, wf));
+        o.y = __float_as_uint(decode_f32(A[4 * q + 1], we, wf));
+        o.z = __float_as_uint(decode_f32(A[4 * q + 2], we, wf));
+        o.w = __float_as_uint(decode_f32(A[4 * q + 3], we, wf));
+      } else {
+        o = make_uint4(A[4 * q], A[4 * q + 1], A[4 * q + 2], A[4 * q + 3]);
+      }
+      out[q] = o;
+    }
+  }
+}
+
+template <bool TO_F32>
+static void launch_unpack_t(int np, const uint32_t* planes, int64_t items, int we, int wf, void* dst,
+                            cudaStream_t s) {
+  int64_t blocks = (items + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  const unsigned b = (unsigned)(blocks < 1 ? 1 : blocks);
+  switch (np) {
+    case 8: unpack_t_kernel<TO_F32, 8><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
+    case 12: unpack_t_kernel<TO_F32, 12><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
+    case 16: unpack_t_kernel<TO_F32, 16><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
+    case 20: unpack_t_kernel<TO_F32, 20><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
+    case 24: unpack_t_kernel<TO_F32, 24><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
+    case 28: unpack_t_kernel<TO_F32, 28><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
+    default: unpack_t_kernel<TO_F32, 32><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
   }
 }
 
@@ -285,17 +383,73 @@ __global__ void __launch_bounds__(256) quantize_acts_kernel(const float* __restr
   const int ni = blockIdx.z / Hp, iyp = blockIdx.z % Hp;
   const int iy = iyp - pad;
   const uint32_t zero_rec = xrec_of(0u, we, wf);
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {  // column within the tile
-    const int ixp = xb + k, ix = ixp - pad, c = cb + threadIdx.x;
-    uint32_t v = zero_rec;
-    if (iy >= 0 && iy < h && ix >= 0 && ix < w && c < cin)
-      v = xrec_of(encode_f32(__ldg(x + (((int64_t)ni * h + iy) * w + ix) * cin + c), we, wf, rnd), we, wf);
-    tile[k][threadIdx.x] = v;
+  // all of this thread's loads first (4 in flight per thread), then the encodes
+  constexpr int K = 32 / 8;  // blockDim.y == 8
+  float xv[K];
+  bool in[K];
+  const int c = cb + threadIdx.x;
+  const bool row_in = iy >= 0 && iy < h && c < cin;
+  const float* __restrict__ xrow = x + ((int64_t)ni * h + iy) * w * cin + c;
+#pragma unroll
+  for (int u = 0; u < K; u++) {  // column within the tile
+    const int ix = xb + threadIdx.y + 8 * u - pad;
+    in[u] = row_in && ix >= 0 && ix < w;
+    xv[u] = in[u] ? __ldg(xrow + (int64_t)ix * cin) : 0.0f;
   }
+#pragma unroll
+  for (int u = 0; u < K; u++)
+    tile[threadIdx.y + 8 * u][threadIdx.x] = in[u] ? xrec_of(encode_f32(xv[u], we, wf, rnd), we, wf) : zero_rec;
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {  // channel within the tile
     const int c = cb + k, ixp = xb + threadIdx.x;
     if (c < cin && ixp < Wp) rec[(((int64_t)ni * cin + c) * Hp + iyp) * Wp + ixp] = tile[threadIdx.x][k];
+  }
+}
+
+// Row-wise variant (the fast path when cin % 4 == 0 and x is 16-byte aligned):
+// one CTA per (image, padded input row) and chunk of CC channels.  Phase 1
+// reads the row's float4 channel quads (consecutive threads = consecutive
+// 16-byte quads: coalesced), encodes them (branch-free encode_f32) and writes
+// the records transposed into shared memory [c][stride]; phase 2 writes each
+// channel's padded record row (Wp words, contiguous in the [n][c][Hp][Wp]
+// layout) with coalesced stores, padding columns / rows as +0 records.
+__global__ void __launch_bounds__(256) quantize_acts_row_kernel(const float* __restrict__ x, int n, int h, int w,
+                                                                int cin, int pad, int we, int wf, int rnd, int cc,
+                                                                int stride, uint32_t* __restrict__ rec) {
+  extern __shared__ uint32_t srec[];  // [cc][stride], stride odd
+  const int Hp = h + 2 * pad, Wp = w + 2 * pad;
+  const int iyp = blockIdx.x, ni = blockIdx.y, c0 = blockIdx.z * cc;
+  const int ncc = min(cc, cin - c0);
+  const int iy = iyp - pad;
+  const uint32_t zero_rec = xrec_of(0u, we, wf);
+  if (iy >= 0 && iy < h) {
+    // thread -> (pixel lane, channel quad) once; no division in the loops
+    const int quads = ncc >> 2;
+    const int ppt = blockDim.x / quads;  // pixels per pass (quads <= 64 when cc <= 256)
+    const int qd = threadIdx.x % quads, ix0 = threadIdx.x / quads;
+    const float4* __restrict__ src = reinterpret_cast<const float4*>(x + (((int64_t)ni * h + iy) * w) * cin + c0);
+    if (ix0 < ppt) {
+      for (int ix = ix0; ix < w; ix += ppt) {
+        const float4 v = __ldg(src + (int64_t)ix * (cin >> 2) + qd);
+        uint32_t* d = srec + (4 * qd) * stride + ix;
+        d[0] = xrec_of(encode_f32(v.x, we, wf, rnd), we, wf);
+        d[stride] = xrec_of(encode_f32(v.y, we, wf, rnd), we, wf);
+        d[2 * stride] = xrec_of(encode_f32(v.z, we, wf, rnd), we, wf);
+        d[3 * stride] = xrec_of(encode_f32(v.w, we, wf, rnd), we, wf);
+      }
+    }
+  }
+  __syncthreads();
+  const bool row_in = iy >= 0 && iy < h;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  uint32_t* __restrict__ dst = rec + (((int64_t)ni * cin + c0) * Hp + iyp) * Wp;
+  for (int c = warp; c < ncc; c += nwarps) {  // one channel row per warp: coalesced stores
+    uint32_t* __restrict__ drow = dst + (int64_t)c * Hp * Wp;
+    const uint32_t* srow = srec + c * stride;
+    for (int ixp = lane; ixp < Wp; ixp += 32) {
+      const int ix = ixp - pad;
+      drow[ixp] = (row_in && ix >= 0 && ix < w) ? srow[ix] : zero_rec;
+    }
   }
 }
 
@@ -441,10 +595,14 @@ static hobf_status unpack_common(bool f32, int32_t we, int32_t wf, const uint32_
   if (!planes || !dst || !aligned16(planes)) return HOBF_EINVAL;
   const int np = hobf_nplanes(3 + we + wf);
   const int64_t items = rows * ((c + 31) / 32);
-  if (f32)
+  if ((c & 31) == 0 && aligned16(dst) && np >= 8) {  // dense rows: thread-per-group transpose
+    if (f32) launch_unpack_t<true>(np, planes, items, we, wf, dst, (cudaStream_t)stream);
+    else launch_unpack_t<false>(np, planes, items, we, wf, dst, (cudaStream_t)stream);
+  } else if (f32) {
     unpack_kernel<true><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(planes, rows, c, we, wf, np, dst);
-  else
+  } else {
     unpack_kernel<false><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(planes, rows, c, we, wf, np, dst);
+  }
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;
@@ -643,9 +801,18 @@ hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, i
   if (!d_x || !d_xrec) return HOBF_EINVAL;
   const int Hp = h + 2 * pad, Wp = w + 2 * pad;
   if ((int64_t)n * Hp > 2147483647LL) return HOBF_EINVAL;
-  dim3 grid((unsigned)((Wp + 31) / 32), (unsigned)((cin + 31) / 32), (unsigned)(n * Hp));
-  quantize_acts_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(d_x, n, h, w, cin, pad, f.we, f.wf, f.round,
-                                                                      d_xrec);
+  const int stride = w | 1;  // odd smem row stride: the transposed writes spread over the banks
+  const int cc = (int)std::min<int64_t>(std::min<int64_t>(cin, 256),
+                                        std::max<int64_t>(4, (32 * 1024 / 4) / stride) / 4 * 4);
+  if ((cin & 3) == 0 && aligned16(d_x) && n <= 65535 && Hp <= 2147483647) {
+    dim3 grid((unsigned)Hp, (unsigned)n, (unsigned)((cin + cc - 1) / cc));
+    quantize_acts_row_kernel<<<grid, 256, (size_t)cc * stride * 4, (cudaStream_t)stream>>>(
+        d_x, n, h, w, cin, pad, f.we, f.wf, f.round, cc, stride, d_xrec);
+  } else {
+    dim3 grid((unsigned)((Wp + 31) / 32), (unsigned)((cin + 31) / 32), (unsigned)(n * Hp));
+    quantize_acts_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(d_x, n, h, w, cin, pad, f.we, f.wf,
+                                                                        f.round, d_xrec);
+  }
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;
