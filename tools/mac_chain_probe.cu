@@ -7,9 +7,14 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef PROBE_FMT
+#define PROBE_FMT F_e5m3_rne
 #include "hobf_circuit_e5m3_rne.cuh"
+#else
+#include PROBE_HDR
+#endif
 
-using F = hobf_gen::F_e5m3_rne;
+using F = hobf_gen::PROBE_FMT;
 
 // MODE 0: operands mutated in registers; 1: + EA/SX mutated too (no hoisting);
 // 2: + table entry gathered from an L1-resident table every MAC (like the conv).
@@ -133,6 +138,11 @@ int main() {
   static uint32_t h[32 * 64 * 16 + 1024];
   for (int i = 0; i < 32 * 64 * 16 + 1024; i++) h[i] = 0x9E3779B9u * (i + 1);
   cudaMemcpy(din, h, sizeof(h), cudaMemcpyHostToDevice);
+#ifdef PROBE_HDR  // wide formats: lone-warp ceiling of the circuit (no register cap)
+  for (int b : {148, 296, 592}) run<1, 1, 1>(b, 500, d, din);
+  for (int b : {148, 296, 592}) run<1, 1, 2>(b, 500, d, din);
+  return 0;
+#endif
   for (int b : {148, 1332}) run<1, 9, 1>(b, 2000, d, din);
   for (int b : {148, 296, 592, 1184}) run<1, 8, 4>(b, 2000, d, din);
   for (int b : {148, 296, 592, 1184}) run<1, 8, 6>(b, 2000, d, din);
