@@ -349,28 +349,70 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
       }
     }
   } else {
-    // ring of PD taps whose operands are loaded; the record of tap t+PD is one further ahead
-    const int taps = a.cin * a.kh * KW;
-    TabTap<F> q[PD > 0 ? PD : 1];
-    TapIter tt, tr;  // tap of the next table entry to load / of the next record to load
+    if constexpr (NT == 32) {  // latency-bound (one warp per CTA): static rings, no register rotation
+      // ring of R = PD + 1 operand slots: the MAC of tap t reads slot t % R while
+      // the table entry of tap t + PD is loaded into slot (t + PD) % R, and the
+      // record of tap t + PD + R (which that load will need R taps later) into
+      // record slot (t + PD) % R.  The loop is unrolled by R so every slot index
+      // is static (modulo variable expansion): no register move rotates a ring --
+      // a move of a slot still being loaded would wait for the load and defeat
+      // the prefetch.
+      constexpr int R = PD + 1;
+      const int taps = a.cin * a.kh * KW;
+      TabTap<F> q[R];
+      uint32_t rq[R];
+      TapIter tt, tr;  // tap of the next table entry to load / of the next record to load
 #pragma unroll
-    for (int i = 0; i < PD; i++) {
-      if (tt.c < a.cin) q[i].load(rec_at(tt.c, tt.kh, tt.kw), tblock(tt.c, tt.kh, tt.kw), a);
-      tt.next(a.kh, KW);
-    }
-    tr = tt;
-    uint32_t rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
-    tr.next(a.kh, KW);
+      for (int i = 0; i < PD; i++) {
+        if (tt.c < a.cin) q[i].load(rec_at(tt.c, tt.kh, tt.kw), tblock(tt.c, tt.kh, tt.kw), a);
+        tt.next(a.kh, KW);
+      }
+      tr = tt;
+#pragma unroll
+      for (int i = 0; i < R; i++) {  // records of taps PD .. PD + R - 1 -> slots (PD + i) % R
+        rq[(PD + i) % R] = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+        tr.next(a.kh, KW);
+      }
+      auto step = [&](TabTap<F>& use, TabTap<F>& fill, uint32_t& rslot) {
+        if (tt.c < a.cin) fill.load(rslot, tblock(tt.c, tt.kh, tt.kw), a);
+        tt.next(a.kh, KW);
+        rslot = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+        tr.next(a.kh, KW);
+        F::mac_tab(acc, use.T, use.EA, use.SX);
+      };
+      int t = 0;
 #pragma unroll 1
-    for (int t = 0; t < taps; t++) {
-      TabTap<F> cur = q[0];
+      for (; t + R <= taps; t += R) {
 #pragma unroll
-      for (int i = 0; i + 1 < PD; i++) q[i] = q[i + 1];
-      if (tt.c < a.cin) q[PD - 1].load(rn, tblock(tt.c, tt.kh, tt.kw), a);
-      tt.next(a.kh, KW);
-      rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+        for (int i = 0; i < R; i++) step(q[i], q[(i + PD) % R], rq[(i + PD) % R]);
+      }
+#pragma unroll
+      for (int i = 0; i < R; i++)
+        if (t + i < taps) step(q[i], q[(i + PD) % R], rq[(i + PD) % R]);
+    } else {  // throughput configs with large tables: rotating ring (measured faster there)
+      // ring of PD taps whose operands are loaded; the record of tap t+PD is one further ahead
+      const int taps = a.cin * a.kh * KW;
+      TabTap<F> q[PD > 0 ? PD : 1];
+      TapIter tt, tr;  // tap of the next table entry to load / of the next record to load
+#pragma unroll
+      for (int i = 0; i < PD; i++) {
+        if (tt.c < a.cin) q[i].load(rec_at(tt.c, tt.kh, tt.kw), tblock(tt.c, tt.kh, tt.kw), a);
+        tt.next(a.kh, KW);
+      }
+      tr = tt;
+      uint32_t rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
       tr.next(a.kh, KW);
-      F::mac_tab(acc, cur.T, cur.EA, cur.SX);
+#pragma unroll 1
+      for (int t = 0; t < taps; t++) {
+        TabTap<F> cur = q[0];
+#pragma unroll
+        for (int i = 0; i + 1 < PD; i++) q[i] = q[i + 1];
+        if (tt.c < a.cin) q[PD - 1].load(rn, tblock(tt.c, tt.kh, tt.kw), a);
+        tt.next(a.kh, KW);
+        rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+        tr.next(a.kh, KW);
+        F::mac_tab(acc, cur.T, cur.EA, cur.SX);
+      }
     }
   }
   F::canon(acc, acc);  // the chain keeps a relaxed accumulator (fpgen.build_mac_tab)
