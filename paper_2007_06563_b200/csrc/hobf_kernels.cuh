@@ -628,9 +628,9 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     // one-warp CTAs (so every SM gets work) running the software-pipelined kernel;
     // otherwise the tables staged in shared memory when a channel block pair fits
     // (wF <= 5 for 3x3), else the L1-served kernels: prefetching one tap ahead when
-    // the table rows do not stay L1 resident (wF >= 8), or three kernel rows per
+    // the table rows do not stay L1 resident (wF >= 6, measured on C5), or three kernel rows per
     // unrolled loop body at <= 64 registers.
-    variant = warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : (F::WF >= 8 ? 4 : (k3 ? 6 : 3));
+    variant = warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : (F::WF >= 6 ? 4 : (k3 ? 6 : 3));
   }
   if (variant == 7 && !smem_ok) variant = 6;
   if (variant == 7) {
