@@ -133,8 +133,8 @@ __device__ __forceinline__ void store_out(const uint32_t* acc, const ConvArgs& a
 // the lanes.  The accumulator (NOUT registers) stays in registers for
 // the whole serial (c, kh, kw) reduction (L10); ReLU is fused (L12).
 // ---------------------------------------------------------------------------
-template <class F>
-__global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
+template <class F, int MINB = 1, bool K33 = false>
+__global__ void __launch_bounds__(128, MINB) conv_direct_kernel(ConvArgs a) {
   const int G = (a.cout + 31) >> 5;
   const int CG = (a.cin + 31) >> 5;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -152,38 +152,49 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvArgs a) {
   const uint32_t* __restrict__ xbase = a.x + ni * (int64_t)a.h * a.w * CG * F::NPI;
   const uint32_t* __restrict__ wbase = a.wt + (int64_t)g * F::NPI;
   const int64_t wstride_c = (int64_t)G * F::NPI;  // next input channel
+  // one tap: the activation's planes broadcast from lane bit (c mod 32), the weight's planes
+  auto tap = [&](int c, int kh, int kw) {
+    const int cg = c >> 5;
+    const uint32_t lift = c_lift[c & 31];  // bit c%32 -> bit 31 (multiply on the FMA pipe)
+    const int iy = oy * a.stride - a.pad + kh, ix = ox * a.stride - a.pad + kw;
+    uint32_t X[F::NPI];
+    if (iy >= 0 && iy < a.h && ix >= 0 && ix < a.w) {
+      const uint4* px = reinterpret_cast<const uint4*>(xbase + (((int64_t)iy * a.w + ix) * CG + cg) * F::NPI);
+#pragma unroll
+      for (int q = 0; q < F::NPI / 4; q++) {
+        const uint4 v = __ldg(px + q);
+        X[4 * q + 0] = v.x; X[4 * q + 1] = v.y; X[4 * q + 2] = v.z; X[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int j = 0; j < F::NPI; j++) X[j] = bcast_bit(X[j], lift, a.one);  // broadcast
+    } else {
+#pragma unroll
+      for (int j = 0; j < F::NPI; j++) X[j] = 0u;  // zero padding = +0 (L11, L14)
+    }
+    uint32_t W[F::NPI];
+    const uint4* pw = reinterpret_cast<const uint4*>(wbase + ((int64_t)(kh * a.kw + kw) * a.cin + c) * wstride_c);
+#pragma unroll
+    for (int q = 0; q < F::NPI / 4; q++) {
+      const uint4 v = __ldg(pw + q);
+      W[4 * q + 0] = v.x; W[4 * q + 1] = v.y; W[4 * q + 2] = v.z; W[4 * q + 3] = v.w;
+    }
+    F::mac(acc, X, W);
+  };
+  if constexpr (K33) {  // the channel's nine taps in one unrolled body (more independent work in view)
 #pragma unroll 1
-  for (int c = 0; c < a.cin; c++) {
-    const int cg = c >> 5, b = c & 31;
-    const uint32_t lift = c_lift[b];  // bit b -> bit 31 (multiply on the FMA pipe)
+    for (int c = 0; c < a.cin; c++) {
+#pragma unroll
+      for (int kh = 0; kh < 3; kh++)
+#pragma unroll
+        for (int kw = 0; kw < 3; kw++) tap(c, kh, kw);
+    }
+  } else {
 #pragma unroll 1
-    for (int kh = 0; kh < a.kh; kh++) {
-      const int iy = oy * a.stride - a.pad + kh;
+    for (int c = 0; c < a.cin; c++) {
 #pragma unroll 1
-      for (int kw = 0; kw < a.kw; kw++) {
-        const int ix = ox * a.stride - a.pad + kw;
-        uint32_t X[F::NPI];
-        if (iy >= 0 && iy < a.h && ix >= 0 && ix < a.w) {
-          const uint4* px = reinterpret_cast<const uint4*>(xbase + (((int64_t)iy * a.w + ix) * CG + cg) * F::NPI);
-#pragma unroll
-          for (int q = 0; q < F::NPI / 4; q++) {
-            const uint4 v = __ldg(px + q);
-            X[4 * q + 0] = v.x; X[4 * q + 1] = v.y; X[4 * q + 2] = v.z; X[4 * q + 3] = v.w;
-          }
-#pragma unroll
-          for (int j = 0; j < F::NPI; j++) X[j] = bcast_bit(X[j], lift, a.one);  // broadcast
-        } else {
-#pragma unroll
-          for (int j = 0; j < F::NPI; j++) X[j] = 0u;  // zero padding = +0 (L11, L14)
-        }
-        uint32_t W[F::NPI];
-        const uint4* pw = reinterpret_cast<const uint4*>(wbase + ((int64_t)(kh * a.kw + kw) * a.cin + c) * wstride_c);
-#pragma unroll
-        for (int q = 0; q < F::NPI / 4; q++) {
-          const uint4 v = __ldg(pw + q);
-          W[4 * q + 0] = v.x; W[4 * q + 1] = v.y; W[4 * q + 2] = v.z; W[4 * q + 3] = v.w;
-        }
-        F::mac(acc, X, W);
+      for (int kh = 0; kh < a.kh; kh++) {
+#pragma unroll 1
+        for (int kw = 0; kw < a.kw; kw++) tap(c, kh, kw);
       }
     }
   }
@@ -605,7 +616,10 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   if (a.items == 0) return cudaSuccess;
   const int threads = 128;
   const int64_t blocks = (a.items + threads - 1) / threads;
-  conv_direct_kernel<F><<<(unsigned)blocks, threads, 0, s>>>(a);
+  if (a.kh == 3 && a.kw == 3 && a.variant != 3)
+    conv_direct_kernel<F, 6, true><<<(unsigned)blocks, threads, 0, s>>>(a);
+  else
+    conv_direct_kernel<F><<<(unsigned)blocks, threads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
