@@ -648,7 +648,7 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   }
   if (variant == 7 && !smem_ok) variant = 6;
   if (variant == 7) {
-    const int sm = a.smem_cfg;  // development override (HOBF_SMEM_CFG): 0 auto, 1..4
+    const int sm = a.smem_cfg;  // development override (HOBF_SMEM_CFG): 0 auto, 2 or 3
     // >= 8 warps per SMSP of work: 128-thread CTAs x 8 per SM (one channel block per
     // buffer) when 8 x 2 blocks fit the SM's shared memory; otherwise (fewer warps, or
     // larger blocks) 256-thread CTAs x 4 per SM (measured on C3 / C4 / C5)
@@ -662,10 +662,8 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
       kern<<<grid(nt), nt, (size_t)(2 * cc * blk_bytes), s>>>(a);
     };
     if (k33) {
-      if (cfg == 1) go(conv_tab_smem_kernel<F, 128, 8, 2, true>, 128, 2);
-      else if (cfg == 2) go(conv_tab_smem_kernel<F, 128, 8, 1, true>, 128, 1);
-      else if (cfg == 3) go(conv_tab_smem_kernel<F, 256, 4, 1, true>, 256, 1);
-      else go(conv_tab_smem_kernel<F, 256, 4, 2, true>, 256, 2);
+      if (cfg == 2) go(conv_tab_smem_kernel<F, 128, 8, 1, true>, 128, 1);
+      else go(conv_tab_smem_kernel<F, 256, 4, 1, true>, 256, 1);
     } else {
       go(conv_tab_smem_kernel<F, 256, 4, 1, false>, 256, 1);
     }
