@@ -39,7 +39,7 @@ L2_BYTES = 126 * 1024 * 1024
 def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="hobf", choices=["hobf", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(inputs.CONFIGS))
@@ -420,7 +420,9 @@ def run_gpu(a, dist):
         "dtype": f"e{we}m{wf}->e{we}m{f.wfo} custom FP, bitsliced u32 lop3", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.text}", "format": f"e{we}m{wf}", "round": a.round,
                    "mac_class": "extended" if a.extended else "single", "relu": a.relu, "global_batch": n * dist.world, "per_gpu_batch": n,
-                   "dense_macs_per_step": macs_rank * dist.world, "l2": "flushed (256 MiB write) between timed steps",
+                   "dense_macs_per_step": macs_rank * dist.world,
+                   "valid_tap_macs_per_step": cfg.valid_macs(n) * dist.world,
+                   "l2": "flushed (256 MiB write) between timed steps",
                    "step": (("quantize_activations(x) + conv2d_prepared + unpack_f32(y)" if use_tab else
                               "quantize_pack(x) + conv2d_dw + unpack_f32(y)" if cfg.dw else
                               "quantize_pack(x) + conv2d + unpack_f32(y)") +

@@ -45,6 +45,13 @@ class ConvConfig:
     def wo(self):
         return (self.w + 2 * self.pad - self.kw) // self.stride + 1
 
+    def valid_macs(self, n=None):
+        """MACs whose activation tap lies inside the image (padding taps excluded)."""
+        n = self.n if n is None else n
+        vy = sum(1 for oy in range(self.ho) for k in range(self.kh) if 0 <= oy * self.stride - self.pad + k < self.h)
+        vx = sum(1 for ox in range(self.wo) for k in range(self.kw) if 0 <= ox * self.stride - self.pad + k < self.w)
+        return n * vy * vx * self.cout * (1 if self.dw else self.cin)
+
     def macs(self, n=None):
         """Dense MACs (padding taps counted, ledger L11)."""
         n = self.n if n is None else n
