@@ -276,7 +276,16 @@ static unsigned warp_grid(int64_t items) {
 static const int kTabMaxWf = 10;
 
 // entry planes: product fraction (wfo = wF+1, or 2wF+1 extended) | Epart (wE+2) | S | K0 | K1
-__host__ __device__ static inline int tab_width(int we, int wfo) { return wfo + (we + 2) + 3; }
+// Product-class encoding of an entry: one-hot flags (zero, normal, inf, NaN) when
+// the two extra planes fit the 16-byte-rounded entry, else the 2-bit code K1 K0
+// (gen/fpgen.tab_onehot states the same rule for the circuit that reads it).
+__host__ __device__ static inline bool tab_onehot(int we, int wfo) {
+  const int base = wfo + (we + 2) + 3;
+  return (base + 2 + 3) / 4 == (base + 3) / 4;
+}
+__host__ __device__ static inline int tab_width(int we, int wfo) {
+  return wfo + (we + 2) + (tab_onehot(we, wfo) ? 5 : 3);
+}
 __host__ __device__ static inline int tab_rows(int wf) { return (1 << wf) + 3; }
 
 // One table entry for weight word w (canonical) and table row r (see
@@ -287,7 +296,8 @@ __host__ __device__ static inline int tab_rows(int wf) { return (1 << wf) + 3; }
 //                          wE+2-bit two's complement; the conv adds ea
 //   bit  wF+wE+3           weight sign (the conv XORs the activation sign)
 //   bits wF+wE+4, +5       product class K0, K1 (00 zero, 01 normal, 10 inf,
-//                          11 NaN), exception algebra of S:68 / SURVEY 8(c) mul
+//                          11 NaN), exception algebra of S:68 / SURVEY 8(c) mul;
+//                          or (tab_onehot) bits +4..+7 = zero, normal, inf, NaN flags
 // Rows: r < 2^wF: normal x with fraction r; 2^wF: x zero; +1: x inf; +2: x NaN.
 // Extended class (wfo = 2wF+1): the product fraction is exact (no rounding).
 __device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int wfo, int rnd) {
@@ -297,9 +307,11 @@ __device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int wfo, int rn
   const uint32_t eb = (w >> wf) & ((1u << we) - 1u);
   const uint32_t fb = w & ((1u << wf) - 1u);
   const int sbit = wfo + EW, k0 = sbit + 1, k1 = sbit + 2;
-  const uint32_t NAN_E = (1u << k0) | (1u << k1);
-  const uint32_t INF_E = (1u << k1) | (sw << sbit);
-  const uint32_t ZERO_E = sw << sbit;
+  const bool oh = tab_onehot(we, wfo);  // one-hot: Tzero sbit+1, Tnorm +2, Tinf +3, Tnan +4
+  const uint32_t NAN_E = oh ? (1u << (sbit + 4)) : ((1u << k0) | (1u << k1));
+  const uint32_t INF_E = (oh ? (1u << (sbit + 3)) : (1u << k1)) | (sw << sbit);
+  const uint32_t ZERO_E = (oh ? (1u << (sbit + 1)) : 0u) | (sw << sbit);
+  const uint32_t NORM_FLAG = oh ? (1u << (sbit + 2)) : (1u << k0);
   const int nrows = 1 << wf;
   if (r == nrows) return (exc & 2u) ? NAN_E : ZERO_E;                  // x = 0: 0*inf, 0*NaN = NaN
   if (r == nrows + 1) return (exc == 0u || exc == 3u) ? NAN_E : INF_E;  // x = inf: inf*0 = NaN
@@ -324,7 +336,7 @@ __device__ uint32_t tab_entry(uint32_t w, int r, int we, int wf, int wfo, int rn
   const uint32_t frac = kept - (1u << wfo);
   const int bias = (1 << (we - 1)) - 1;
   const uint32_t ep = (uint32_t)((int)eb - bias + (int)inc) & ((1u << EW) - 1u);
-  return frac | (ep << wfo) | (sw << sbit) | (1u << k0);
+  return frac | (ep << wfo) | (sw << sbit) | NORM_FLAG;
 }
 
 // Activation records for hobf_conv2d_prepared: one uint32 per element in a

@@ -480,11 +480,20 @@ def build_relu(we, w) -> Circuit:
 
 # --------------------------------------------------------------------------- weight-table MAC
 
+def tab_onehot(we: int, wfo: int) -> bool:
+    """Product-class encoding of a table entry: one-hot flags (zero, normal, inf,
+    NaN: 4 planes, 3 lop3 fewer per MAC) when they fit the padding of the
+    16-byte-rounded entry, else the 2-bit class code K1 K0 (no wider entry)."""
+    base = wfo + (we + 2) + 3
+    return (base + 2 + 3) // 4 == (base + 3) // 4
+
+
 def tab_entry_width(we: int, wf: int, wfo: int | None = None) -> int:
-    """Planes of one weight-table entry: frac (wfo) | Epart (wE+2) | S | K0 | K1;
+    """Planes of one weight-table entry: frac (wfo) | Epart (wE+2) | S | class,
+    class = K0 K1 (2 planes) or Tzero Tnorm Tinf Tnan (4 planes, tab_onehot);
     wfo = wF+1 (single class) or 2wF+1 (extended: the exact product)."""
     wfo = wf + 1 if wfo is None else wfo
-    return wfo + (we + 2) + 3
+    return wfo + (we + 2) + (5 if tab_onehot(we, wfo) else 3)
 
 
 def product_from_table(g: AIG, t, ea, sx, we: int, wf: int, wfo: int | None = None) -> Operand:
@@ -498,8 +507,9 @@ def product_from_table(g: AIG, t, ea, sx, we: int, wf: int, wfo: int | None = No
     holding for every lane the rounded product fraction (round to wF+1 bits at
     the product's own binade, RNE/RTZ), Epart = eb - bias + (normalise +
     round carry) as a wE+2-bit two's complement number, the weight sign and the
-    product class (K1 K0: 00 zero, 01 normal, 10 inf, 11 NaN; rows for x =
-    zero / inf / NaN encode the exception algebra of S:68).  The gates left
+    product class (K1 K0: 00 zero, 01 normal, 10 inf, 11 NaN, or one-hot flags
+    when they fit, tab_onehot; rows for x = zero / inf / NaN encode the
+    exception algebra of S:68).  The gates left
     add the activation exponent, classify overflow / underflow (ledger L5, L6)
     and combine the signs.  Extended class (wfo = 2wF+1): the table holds the
     exact product fraction (no rounding)."""
@@ -507,17 +517,24 @@ def product_from_table(g: AIG, t, ea, sx, we: int, wf: int, wfo: int | None = No
     EW = we + 2
     F = t[0:wfo]
     Ep = t[wfo:wfo + EW]
-    S, K0, K1 = t[wfo + EW], t[wfo + EW + 1], t[wfo + EW + 2]
+    S = t[wfo + EW]
     E = ripple_add(g, Ep, list(ea), FALSE, width=EW)
     unf = E[EW - 1]
     ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])
+    sign = g.XOR(S, sx)
+    if tab_onehot(we, wfo):
+        Tz, Tn, Ti, Tq = t[wfo + EW + 1], t[wfo + EW + 2], t[wfo + EW + 3], t[wfo + EW + 4]
+        norm = g.AND(Tn, g.AND(g.NOT(ovf), g.NOT(unf)))
+        zero = g.OR(Tz, g.AND(Tn, unf))
+        inf = g.OR(Ti, g.AND(Tn, ovf))
+        return Operand(we, wfo, F, E[:we], sign, norm, zero, inf, Tq, g.OR(inf, Tq), canonical=False)
+    K0, K1 = t[wfo + EW + 1], t[wfo + EW + 2]
     nK1 = g.NOT(K1)
     norm = g.AND(g.AND(nK1, K0), g.AND(g.NOT(ovf), g.NOT(unf)))
     zero = g.AND(nK1, g.OR(g.NOT(K0), unf))
     inf = g.OR(g.AND(K1, g.NOT(K0)), g.AND(g.AND(nK1, K0), ovf))
     nan = g.AND(K1, K0)
     special = g.OR(K1, g.AND(K0, ovf))
-    sign = g.XOR(S, sx)
     return Operand(we, wfo, F, E[:we], sign, norm, zero, inf, nan, special, canonical=False)
 
 

@@ -19,6 +19,13 @@ def row_of(x, we, wf):
     return np.where(exc == 1, fa, (1 << wf) + special)
 
 
+def onehot(we, wfo):
+    """Class encoding of an entry: one-hot (zero, normal, inf, NaN flags) when the
+    two extra planes fit the 4-plane-rounded entry, else the 2-bit code K1 K0."""
+    base = wfo + we + 5
+    return -(-(base + 2) // 4) == -(-base // 4)
+
+
 def entries(w, r, we, wf, rnd, wfo=None):
     """wfo = wF+1 (single class, rounded) or 2wF+1 (extended class, exact)."""
     w = np.asarray(w, dtype=np.int64)
@@ -30,9 +37,11 @@ def entries(w, r, we, wf, rnd, wfo=None):
     eb = (w >> wf) & ((1 << we) - 1)
     fb = w & ((1 << wf) - 1)
     sbit = wfo + EW
-    NAN = (1 << (sbit + 1)) | (1 << (sbit + 2))
-    INF = (1 << (sbit + 2)) | (sw << sbit)
-    ZERO = sw << sbit
+    oh = onehot(we, wfo)
+    NAN = (1 << (sbit + 4)) if oh else (1 << (sbit + 1)) | (1 << (sbit + 2))
+    INF = (1 << (sbit + (3 if oh else 2))) | (sw << sbit)
+    ZERO = ((1 << (sbit + 1)) if oh else 0) | (sw << sbit)
+    NORM = 1 << (sbit + (2 if oh else 1))
     nrows = 1 << wf
     # both normal: exact product (1.fa)(1.fb), round to wfo fraction bits at its binade
     ma = (1 << wf) | np.minimum(r, nrows - 1)
@@ -53,7 +62,7 @@ def entries(w, r, we, wf, rnd, wfo=None):
     frac = kept - (1 << wfo)
     bias = (1 << (we - 1)) - 1
     ep = (eb - bias + inc) & ((1 << EW) - 1)
-    normal_e = frac | (ep << wfo) | (sw << sbit) | (1 << (sbit + 1))
+    normal_e = frac | (ep << wfo) | (sw << sbit) | NORM
     out = np.select([exc == 0, exc == 2, exc == 3], [ZERO, INF, NAN], normal_e)
     out = np.where(r == nrows, np.where((exc & 2) != 0, NAN, ZERO), out)
     out = np.where(r == nrows + 1, np.where((exc == 0) | (exc == 3), NAN, INF), out)
