@@ -90,6 +90,30 @@ __device__ __forceinline__ uint32_t encode_f32(float f, int we, int wf, int rnd)
   return ex == 0xFF ? nonfinite : ((ex == 0 && man == 0) ? sfield : finite);
 }
 
+// float32 -> F(we, wf) for we <= 7, wf <= 22 (the activation quantiser's fast
+// path; same results as encode_f32): the rounding to wf fraction bits is done on
+// the float32 bit pattern itself (RNE: add half - 1 + lsb below the cut, then
+// truncate -- a carry out of the mantissa moves into the float exponent, i.e.
+// the value rounds up into the next binade), then the exponent is re-biased and
+// range-checked (overflow -> inf, underflow -> zero keeping the sign; every
+// float32 subnormal underflows because the format's emin >= -63 here).
+__device__ __forceinline__ uint32_t encode_f32_fast(float f, int we, int wf, int rnd) {
+  const uint32_t u = __float_as_uint(f);
+  const int sh = 23 - wf;
+  const uint32_t lsb = (u >> sh) & 1u;
+  const uint32_t ur = rnd == 0 ? u + ((1u << (sh - 1)) - 1u) + lsb : u;
+  const int ex = (int)((u >> 23) & 0xFFu);
+  const int E = (int)((ur >> 23) & 0xFFu) - 127 + ((1 << (we - 1)) - 1);
+  const int top = wf + we + 1;
+  const uint32_t sfield = (u >> 31) << (wf + we);
+  const uint32_t frac = (ur >> sh) & ((1u << wf) - 1u);
+  const uint32_t inf = (2u << top) | sfield;
+  const uint32_t finite = E > (1 << we) - 1 ? inf
+                        : (E < 0 || ex == 0) ? sfield : (1u << top) | sfield | ((uint32_t)E << wf) | frac;
+  const uint32_t nonfinite = (u & 0x7FFFFFu) ? (3u << top) : inf;
+  return ex == 0xFF ? nonfinite : finite;
+}
+
 // F(we, wf) word -> float32 (exact for we <= 7, wf <= 23).  Branch-free: the
 // four exception classes are selected, not branched on (no divergence).
 __device__ __forceinline__ float decode_f32(uint32_t v, int we, int wf) {
@@ -146,8 +170,10 @@ __global__ void __launch_bounds__(256) pack_kernel(const void* __restrict__ src,
     }
     uint32_t v = 0u;
     if (ok) {
-      if (FROM_F32)
-        v = encode_f32(__ldg(reinterpret_cast<const float*>(src) + idx), we, wf, rnd);
+      if (FROM_F32) {
+        const float xf = __ldg(reinterpret_cast<const float*>(src) + idx);
+        v = we <= 7 ? encode_f32_fast(xf, we, wf, rnd) : encode_f32(xf, we, wf, rnd);
+      }
       else
         v = canon_word(__ldg(reinterpret_cast<const uint32_t*>(src) + idx), we, wf);
     }
@@ -444,10 +470,17 @@ __global__ void __launch_bounds__(256) quantize_acts_row_kernel(const float* __r
       for (int ix = ix0; ix < w; ix += ppt) {
         const float4 v = __ldg(src + (int64_t)ix * (cin >> 2) + qd);
         uint32_t* d = srec + (4 * qd) * stride + ix;
-        d[0] = xrec_of(encode_f32(v.x, we, wf, rnd), we, wf);
-        d[stride] = xrec_of(encode_f32(v.y, we, wf, rnd), we, wf);
-        d[2 * stride] = xrec_of(encode_f32(v.z, we, wf, rnd), we, wf);
-        d[3 * stride] = xrec_of(encode_f32(v.w, we, wf, rnd), we, wf);
+        if (we <= 7) {
+          d[0] = xrec_of(encode_f32_fast(v.x, we, wf, rnd), we, wf);
+          d[stride] = xrec_of(encode_f32_fast(v.y, we, wf, rnd), we, wf);
+          d[2 * stride] = xrec_of(encode_f32_fast(v.z, we, wf, rnd), we, wf);
+          d[3 * stride] = xrec_of(encode_f32_fast(v.w, we, wf, rnd), we, wf);
+        } else {
+          d[0] = xrec_of(encode_f32(v.x, we, wf, rnd), we, wf);
+          d[stride] = xrec_of(encode_f32(v.y, we, wf, rnd), we, wf);
+          d[2 * stride] = xrec_of(encode_f32(v.z, we, wf, rnd), we, wf);
+          d[3 * stride] = xrec_of(encode_f32(v.w, we, wf, rnd), we, wf);
+        }
       }
     }
   }
