@@ -289,6 +289,63 @@ static void launch_unpack_t(int np, const uint32_t* planes, int64_t items, int w
   }
 }
 
+// Pack, one thread per 32-lane group (the fast path for dense rows): the 32
+// consecutive source elements arrive as eight 128-bit loads, are encoded /
+// canonicalised in registers, and the register bit transpose turns the 32 words
+// into the group's plane words, stored as NP / 4 128-bit stores.
+template <bool FROM_F32, int NP>
+__global__ void __launch_bounds__(256) pack_t_kernel(const void* __restrict__ src, int64_t items, int we, int wf,
+                                                     int rnd, uint32_t* __restrict__ planes) {
+  const int nb = 3 + we + wf;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t A[32];
+    const uint4* in = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(src) + it * 32);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint4 v = __ldg(in + q);
+      A[4 * q] = v.x; A[4 * q + 1] = v.y; A[4 * q + 2] = v.z; A[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int l = 0; l < 32; l++) {
+      if (FROM_F32) {
+        const float xf = __uint_as_float(A[l]);
+        A[l] = we <= 7 ? encode_f32_fast(xf, we, wf, rnd) : encode_f32(xf, we, wf, rnd);
+      } else {
+        A[l] = canon_word(A[l], we, wf);
+      }
+    }
+    transpose32(A);  // A[j] = plane j: bit l = field bit j of lane l
+    uint4* out = reinterpret_cast<uint4*>(planes + it * NP);
+#pragma unroll
+    for (int q = 0; q < NP / 4; q++) {
+      uint4 o;
+      o.x = 4 * q < nb ? A[4 * q] : 0u;
+      o.y = 4 * q + 1 < nb ? A[4 * q + 1] : 0u;
+      o.z = 4 * q + 2 < nb ? A[4 * q + 2] : 0u;
+      o.w = 4 * q + 3 < nb ? A[4 * q + 3] : 0u;
+      out[q] = o;
+    }
+  }
+}
+
+template <bool FROM_F32>
+static void launch_pack_t(int np, const void* src, int64_t items, int we, int wf, int rnd, uint32_t* planes,
+                          cudaStream_t s) {
+  int64_t blocks = (items + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  const unsigned b = (unsigned)(blocks < 1 ? 1 : blocks);
+  switch (np) {
+    case 8: pack_t_kernel<FROM_F32, 8><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+    case 12: pack_t_kernel<FROM_F32, 12><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+    case 16: pack_t_kernel<FROM_F32, 16><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+    case 20: pack_t_kernel<FROM_F32, 20><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+    case 24: pack_t_kernel<FROM_F32, 24><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+    case 28: pack_t_kernel<FROM_F32, 28><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+    default: pack_t_kernel<FROM_F32, 32><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+  }
+}
+
 static unsigned warp_grid(int64_t items) {
   int64_t blocks = (items + 7) / 8;  // 8 warps per 256-thread block
   const int64_t cap = 148 * 16;
@@ -612,10 +669,14 @@ static hobf_status pack_common(bool f32, int32_t we, int32_t wf, int32_t rnd, co
   if (!src || !planes || !aligned16(planes)) return HOBF_EINVAL;
   const int np = hobf_nplanes(3 + we + wf);
   const int64_t items = rows * ((c + 31) / 32);
-  if (f32)
+  if ((c & 31) == 0 && aligned16(src) && np >= 8) {  // dense rows: thread-per-group transpose
+    if (f32) launch_pack_t<true>(np, src, items, we, wf, rnd, planes, (cudaStream_t)stream);
+    else launch_pack_t<false>(np, src, items, we, wf, 0, planes, (cudaStream_t)stream);
+  } else if (f32) {
     pack_kernel<true><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(src, rows, c, we, wf, rnd, np, planes);
-  else
+  } else {
     pack_kernel<false><<<warp_grid(items), 256, 0, (cudaStream_t)stream>>>(src, rows, c, we, wf, 0, np, planes);
+  }
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
   return HOBF_OK;
