@@ -255,7 +255,60 @@ def map_aig(aig, outputs: list[int], passes: int = 4, max_cuts: int = 24) -> Map
         if kind[v] == "and" and refs[v] > 0:
             c = chosen[v]
             luts.append((v, c.leaves, _full(c.tt, len(c.leaves))))
+    luts = absorb_small_luts(luts, outputs)
     return Mapping(aig, outputs, luts, chosen)
+
+
+def _eval_tt(tt: int, vals) -> int:
+    idx = 0
+    for i, x in enumerate(vals):
+        idx |= (x & 1) << i
+    return (tt >> idx) & 1
+
+
+def absorb_small_luts(luts, outputs):
+    """Post-pass: a LUT f that is not an output and whose every consumer can take
+    f's leaves directly (the consumer's other leaves plus f's leaves number at
+    most 3) is folded into all its consumers and removed -- one lop3 fewer.
+    Local area recovery cannot find this when f has several consumers (freeing
+    f needs all of them to move at once).  Repeated until no LUT qualifies."""
+    lut = {v: (tuple(leaves), tt) for v, leaves, tt in luts}
+    order = [v for v, _, _ in luts]
+    out_nodes = {o >> 1 for o in outputs}
+    changed = True
+    while changed:
+        changed = False
+        fan = {}
+        for v in order:
+            for l in lut[v][0]:
+                if l in lut:
+                    fan.setdefault(l, []).append(v)
+        for f in order:
+            if f in out_nodes or f not in fan:
+                continue
+            fl, ftt = lut[f]
+            new = {}
+            for g in fan[f]:
+                gl, gtt = lut[g]
+                nl = tuple(sorted(set(x for x in gl if x != f) | set(fl)))
+                if len(nl) > 3:
+                    new = None
+                    break
+                tt = 0
+                for k in range(8):
+                    val = {x: (k >> i) & 1 for i, x in enumerate(nl)}
+                    fv = _eval_tt(ftt, [val[x] for x in fl])
+                    if _eval_tt(gtt, [fv if x == f else val[x] for x in gl]):
+                        tt |= 1 << k
+                new[g] = (nl, tt)
+            if not new:
+                continue
+            lut.update(new)
+            del lut[f]
+            order.remove(f)
+            changed = True
+            break
+    return [(v, lut[v][0], lut[v][1]) for v in order]
 
 
 def lop3_eval(imm: int, a, b, c, ones):
