@@ -275,6 +275,39 @@ __global__ void __launch_bounds__(128) conv_dw_kernel(ConvArgs a) {
 // ---------------------------------------------------------------------------
 // Per-tap operands of the table MAC: broadcast activation exponent / sign
 // planes (FMA pipe) and the table entry the activation's row selects.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// The TAB_W live planes of a table entry: 128-bit loads for full quads, a 64-
+// and / or 32-bit load for the tail -- never a load into a dead register.  (A
+// 128-bit load whose last register is dead lets ptxas reuse that register at
+// once; the reuse then waits on the load in flight, which cost the latency-bound
+// schedule half its speed.)  Planes past TAB_W are never read by the circuit.
+template <class F, bool GLOBAL = true>
+__device__ __forceinline__ void load_entry(uint32_t (&T)[F::NPT], const uint32_t* __restrict__ p, int zero) {
+  constexpr int W = F::TAB_W;
+  const uint4* p4 = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int q = 0; q < W / 4; q++) {
+    const uint4 v = GLOBAL ? __ldg(p4 + q) : p4[q];
+    T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
+  }
+  // the tail as separate narrower loads; the last word's address goes through a
+  // run-time zero so that neither the compiler nor ptxas can prove the loads
+  // adjacent and merge them back into one 128-bit load with a dead register
+  constexpr int b = W / 4 * 4;
+  if constexpr (W - b >= 2) {
+    const uint2* p2 = reinterpret_cast<const uint2*>(p + b);
+    const uint2 v = GLOBAL ? __ldg(p2) : *p2;
+    T[b] = v.x; T[b + 1] = v.y;
+  }
+  if constexpr ((W - b) & 1) {
+    const uint32_t* pl = p + W - 1 + zero;
+    T[W - 1] = GLOBAL ? __ldg(pl) : *pl;
+  }
+#pragma unroll
+  for (int j = W; j < F::NPT; j++) T[j] = 0u;
+}
+
 template <class F>
 struct TabTap {
   uint32_t EA[F::WE], SX[1], T[F::NPT];
@@ -284,12 +317,7 @@ struct TabTap {
     for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
     SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
     const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
-    const uint4* pt4 = reinterpret_cast<const uint4*>(tblock + (int64_t)row * tab_stride(F::NPT, F::WF));
-#pragma unroll
-    for (int q = 0; q < F::NPT / 4; q++) {
-      const uint4 v = __ldg(pt4 + q);
-      T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
-    }
+    load_entry<F>(T, tblock + (int64_t)row * tab_stride(F::NPT, F::WF), a.one - 1);
   }
 };
 
@@ -447,7 +475,6 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
 // kernel row's records prefetched).  Same circuit, same serial (c, kh, kw)
 // order as conv_tab_kernel: identical results.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
@@ -492,12 +519,7 @@ __device__ __forceinline__ void smem_tap(uint32_t* acc, uint32_t rec, const uint
   for (int j = 0; j < WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + j]), a.one);
   SX[0] = (uint32_t)__mulhi((int32_t)(rec * a.lift[WF + WE]), a.one);
   const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
-  const uint4* pt4 = reinterpret_cast<const uint4*>(tblk + (int)row * S);
-#pragma unroll
-  for (int q = 0; q < F::NPT / 4; q++) {
-    const uint4 v = pt4[q];
-    T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
-  }
+  load_entry<F, false>(T, tblk + (int)row * S, a.one - 1);
   F::mac_tab(acc, T, EA, SX);
 }
 
