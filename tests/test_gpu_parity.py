@@ -33,25 +33,47 @@ def special_floats():
 
 # ----------------------------------------------------------------------------- quantise / pack / unpack
 
-@pytest.mark.parametrize("we,wf", [(5, 10), (5, 3), (4, 3), (6, 2), (4, 10), (6, 9), (5, 2)])
+@pytest.mark.parametrize("we,wf", [(5, 10), (5, 3), (4, 3), (6, 2), (4, 10), (6, 9), (5, 2), (7, 12), (8, 7), (2, 1)])
 @pytest.mark.parametrize("rnd", [0, 1])
 def test_quantize_pack_unpack_matches_oracle_encode(we, wf, rnd):
+    """Both pack / unpack paths: ragged rows (warp-ballot kernels) and dense rows
+    (C % 32 == 0: thread-per-group register transpose), the float32 fast
+    quantiser (we <= 7) and the general one (we = 8)."""
     H = hobf()
     rng = np.random.default_rng(we * 100 + wf + rnd)
     x = (rng.standard_normal(50_000) * np.exp(rng.uniform(-25, 25, 50_000))).astype(np.float32)
     x = np.concatenate([x, special_floats()])
-    for rows, c in [(x.size // 50, 50), (1, x.size), (x.size // 20, 20)]:
+    for rows, c in [(x.size // 50, 50), (1, x.size), (x.size // 20, 20), (x.size // 64, 64), (x.size // 32, 32),
+                    (1, x.size // 32 * 32)]:
         xx = x[: rows * c].reshape(rows, c)
         planes = H.quantize_pack(we, wf, torch.from_numpy(xx).cuda(), rnd)
         got = to_np_words(H.unpack(we, wf, planes, rows, c))
         exp = oracle.encode_f32(xx, we, wf, rnd)
         assert np.array_equal(got, exp)
+        if we > 7:  # float32 holds every F(we <= 7, wf <= 23) value exactly; unpack_f32 refuses we = 8
+            with pytest.raises(H.HobfError):
+                H.unpack_f32(we, wf, planes, rows, c)
+            continue
         # unpack to float32 is the exact decoded value
         f = H.unpack_f32(we, wf, planes, rows, c).cpu().numpy()
         dec = oracle.decode_f64(exp, we, wf)
         both_nan = np.isnan(f) & np.isnan(dec)
         assert np.array_equal(f[~both_nan].astype(np.float64), dec[~both_nan])
         assert np.array_equal(np.signbit(f[~both_nan]), np.signbit(dec[~both_nan]))
+
+
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 10), (6, 5)])
+def test_pack_canonicalises_dense_rows(we, wf):
+    """The thread-per-group pack / unpack (C % 32 == 0) canonicalise like the ragged path."""
+    H = hobf()
+    rng = np.random.default_rng(12)
+    rows, c = 257, 96
+    raw = rng.integers(0, 1 << 32, (rows, c), dtype=np.uint64).astype(np.uint32)
+    planes = H.pack(we, wf, to_dev_words(raw))
+    got = to_np_words(H.unpack(we, wf, planes, rows, c))
+    nb = 3 + we + wf
+    assert np.array_equal(got, oracle.canon(raw & np.uint32((1 << nb) - 1), we, wf))
+    assert np.all(to_np_words(planes)[:, :, nb:] == 0)
 
 
 @pytest.mark.parametrize("we,wf", [(5, 3), (4, 10), (6, 5)])
