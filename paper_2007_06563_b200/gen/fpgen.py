@@ -171,7 +171,7 @@ def lzc(g: AIG, v):
     return cnt, z
 
 
-def normalize_left(g: AIG, v, max_shift=None):
+def normalize_left(g: AIG, v, max_shift=None, low_zero=(0, 0)):
     """Leading-zero normalisation by successive detection: for 2^j from the
     largest power of two down, if the top 2^j bits of the current vector are
     all zero, shift it left by 2^j.  Returns (normalised v, shift count bits
@@ -180,7 +180,11 @@ def normalize_left(g: AIG, v, max_shift=None):
     ``max_shift``: a bound on the shift any nonzero input needs (its leading
     one is never below bit L-1-max_shift); only bitlen(max_shift) stages are
     built.  all_zero stays exact: a nonzero input always ends with its leading
-    one at the top."""
+    one at the top.
+
+    ``low_zero = (nbits, min_shift)``: whenever a stage shifting by >= min_shift
+    shifts, the input's low nbits are zero (an invariant of the caller), so
+    those output bits pass through without a gate."""
     L = len(v)
     K = 0
     if max_shift is None:
@@ -193,7 +197,8 @@ def normalize_left(g: AIG, v, max_shift=None):
         sh = 1 << j
         zj = g.NOT(g.OR_many(cur[L - sh:]))
         cnt[j] = zj
-        cur = [g.MUX(zj, cur[i - sh] if i - sh >= 0 else FALSE, cur[i]) for i in range(L)]
+        nlow = low_zero[0] if sh >= low_zero[1] > 0 else 0
+        cur = [cur[i] if i < nlow else g.MUX(zj, cur[i - sh] if i - sh >= 0 else FALSE, cur[i]) for i in range(L)]
     return cur, cnt, g.NOT(cur[L - 1])
 
 
@@ -361,7 +366,9 @@ def fp_add_ops(g: AIG, A: Operand, B: Operand, rnd: int, shift_order="small_firs
         # the aligned Y has no bits below position 2 (its LSB lands on the G
         # position at most), so the exact sum is a multiple of 2^2 and a
         # nonzero Z has its leading one at bit >= 2: shift <= W - 1 = p + 1.
-        Zn, cnt, zsum = normalize_left(g, Z, max_shift=W - 1)
+        # A shift of >= 3 happens only for d <= 1 (or an all-zero sum), where the
+        # aligned Y has no bits below position 2: Z[0] = Z[1] = 0 then.
+        Zn, cnt, zsum = normalize_left(g, Z, max_shift=W - 1, low_zero=(2, 3))
     else:
         cnt, zsum = lzc(g, Z)
         Zn = shift_left(g, Z, cnt)
