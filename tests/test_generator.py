@@ -285,3 +285,34 @@ def test_extended_mac_and_mac_tab_random(we, wf, rnd):
     ct = fpgen.build_mac_tab(we, wf, rnd, wfo)
     _check(ct, lutmap.map_aig(ct.g, ct.outputs), tabref.circuit_inputs(tabref.relax(acc, we, wfo, rng), x, w, we, wf, rnd, wfo),
            exp, lambda v: tabref.canon(v, we, wfo))
+
+
+def test_absorb_post_pass_preserves_function_and_never_adds_luts():
+    """The mapper's post-pass (fold a LUT into all its consumers when each can take
+    its leaves) on random AIGs: the mapped network computes the same outputs as
+    the AIG, with no more LUTs than the mapping without the pass."""
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        g = aigmod.AIG()
+        ins = g.inputs("x", 6)
+        pool = list(ins)
+        for _ in range(int(rng.integers(10, 40))):
+            a, b, c = (pool[int(rng.integers(0, len(pool)))] ^ int(rng.integers(0, 2)) for _ in range(3))
+            op = int(rng.integers(0, 4))
+            pool.append([g.AND(a, b), g.XOR(a, b), g.MUX(a, b, c), g.MAJ(a, b, c)][op])
+        outs = [pool[-1 - int(k)] ^ int(rng.integers(0, 2)) for k in rng.choice(min(8, len(pool) - 6), 3, replace=False)]
+        m = lutmap.map_aig(g, outs)
+        # the same mapping without the post-pass
+        orig = lutmap.absorb_small_luts
+        try:
+            lutmap.absorb_small_luts = lambda luts, outputs: luts
+            m0 = lutmap.map_aig(g, outs)
+        finally:
+            lutmap.absorb_small_luts = orig
+        assert m.n_luts <= m0.n_luts
+        words = {"x": rng.integers(0, 1 << 63, (6, 4), dtype=np.uint64)}
+        words = {f"x[{i}]": words["x"][i] for i in range(6)}
+        ref = g.simulate(words, outs, np)
+        got = lutmap.simulate_mapping(m, words, np)
+        for r, o in zip(ref, got):
+            assert np.array_equal(r, o), trial
