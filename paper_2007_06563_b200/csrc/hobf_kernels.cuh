@@ -638,7 +638,7 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   if (a.items == 0) return cudaSuccess;
   const int threads = 128;
   const int64_t blocks = (a.items + threads - 1) / threads;
-  if (a.kh == 3 && a.kw == 3 && a.variant != 3)
+  if (a.kh == 3 && a.kw == 3)  // the channel's nine taps in one body, <= 80 registers
     conv_direct_kernel<F, 6, true><<<(unsigned)blocks, threads, 0, s>>>(a);
   else
     conv_direct_kernel<F><<<(unsigned)blocks, threads, 0, s>>>(a);
@@ -654,8 +654,8 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const bool k3 = a.kw == 3;
   int variant = a.variant;
   const int64_t warps = (npix + 31) / 32 * gy;
-  // shared-memory table staging (variant 7): CTAs of NT7 threads, buffers of CC7
-  // channel blocks, double-buffered, within the shared memory of 4 (or 8) CTAs / SM
+  // shared-memory table staging (variant 7): one channel block per buffer, double-
+  // buffered; the pair must fit 50 KB so that 4 (256-thread) CTAs share an SM
   const int64_t blk_bytes = (int64_t)tab_block_words<F>(a.kh * a.kw) * 4;
   const bool k33 = k3 && a.kh == 3;
   const bool smem_ok = 2 * blk_bytes <= 50 * 1024;
