@@ -128,7 +128,7 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
  * or -1 if the format has no table kernel (wf > 10, extended class).
  * Layout: [ceil(cout/32)][cin][kh][kw][2^wf + 3 rows][stride] uint32, where an
  * entry has NPT = roundup(wfo + we + 5, 4) planes and rows are padded to
- * stride = NPT + 4 words when wf <= 5 and NPT/4 is even (conflict-free 128-bit
+ * stride = NPT + 4 words when wf <= 7 and NPT/4 is even (conflict-free 128-bit
  * row gathers from shared memory), else stride = NPT; everything one 32-channel output group needs
  * for one input channel is one contiguous block (one bulk copy). */
 int64_t hobf_wtab_words(hobf_fmt f, int32_t kh, int32_t kw, int32_t cin, int32_t cout);
@@ -213,10 +213,13 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
  * with a 3-deep prefetch ring (fewer warps than SMSPs); 6 = three kernel rows
  * (one input channel) per unrolled loop body, <= 64 registers; 7 = the
  * weight-table block of each input channel staged in shared memory by TMA bulk
- * copies (double-buffered, mbarrier completion), 256-thread CTAs -- needs
- * 2 * kh*kw * (2^wf + 3) * stride * 4 bytes <= 50 KB (wf <= 5 for 3x3), else it
- * falls back to variant 6.  Variants 3 and 6 need kw == 3 (others fall back to
- * the generic loop).  Every variant
+ * copies (double-buffered, mbarrier completion), 128/256-thread CTAs -- needs
+ * 2 * kh*kw * (2^wf + 3) * stride * 4 bytes <= 50 KB (wf <= 5 for 3x3), else
+ * it falls back to variant 6; 8 = as 7 with one kernel row (3 taps, wf = 6, 7)
+ * or one tap (wf = 8, 9) of one input channel per staged buffer (3x3 only,
+ * else it falls back to variant 7).
+ * Variants 3 and 6 need kw == 3 (others fall back to the generic loop).  Every
+ * variant
  * runs the same circuit over the same serial (c, kh, kw) order: identical
  * results.  Unknown variants -> HOBF_EINVAL. */
 hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,

@@ -938,7 +938,7 @@ hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t 
                                     uint32_t* d_y_planes, int32_t variant, hobf_stream stream) {
   const uint32_t* d_x_planes = d_xrec;
   g_last_launches = 0;
-  if (variant != 0 && (variant < 3 || variant > 7)) return HOBF_EINVAL;
+  if (variant != 0 && (variant < 3 || variant > 8)) return HOBF_EINVAL;
   if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
     return HOBF_EINVAL;
   if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)

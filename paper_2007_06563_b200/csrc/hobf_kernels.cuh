@@ -525,7 +525,11 @@ __device__ __forceinline__ void smem_tap(uint32_t* acc, uint32_t rec, const uint
 
 // CC input channels per staged buffer (one TMA bulk copy of CC contiguous
 // channel blocks); K33: kh = kw = 3, the channel's nine taps fully unrolled.
-template <class F, int NT, int MINB, int CC, bool K33>
+// UT > 0 (K33 only): UT taps of one channel per staged buffer -- 3 = one kernel
+// row, 1 = one tap -- for the formats whose channel block pair does not fit
+// (wF >= 6): the flat unit k = (9 c + 3 kh + kw) / UT is the contiguous slice
+// of UT taps of the group's block.
+template <class F, int NT, int MINB, int CC, bool K33, int UT = 0>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
   extern __shared__ __align__(128) uint32_t smem_tab[];  // [2][CC][kh*kw][rows][stride]
   __shared__ __align__(8) uint64_t full[2];
@@ -543,6 +547,7 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
   const uint32_t blk = (uint32_t)(KHW * R * S);  // words per (group, channel) block
   const uint32_t* __restrict__ gsrc = a.wt + (int64_t)g * a.cin * blk;
   const int nchunks = (a.cin + CC - 1) / CC;
+  constexpr uint32_t UBLK = (uint32_t)UT * R * S;  // UT > 0: words per staged unit
 
   uint32_t acc[F::NOUT];
 #pragma unroll
@@ -559,6 +564,11 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
   }
   __syncthreads();
   auto issue = [&](int k) {  // chunk k -> buffer k & 1
+    if (UT > 0) {
+      mbar_expect_tx(&full[k & 1], UBLK * 4u);
+      bulk_g2s(smem_tab + (k & 1) * UBLK, gsrc + (int64_t)k * UBLK, UBLK * 4u, &full[k & 1]);
+      return;
+    }
     const int c0 = k * CC, cc = min(CC, a.cin - c0);
     const uint32_t bytes = (uint32_t)cc * blk * 4u;
     mbar_expect_tx(&full[k & 1], bytes);
@@ -570,8 +580,46 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
 #pragma unroll
     for (int kw = 0; kw < 3; kw++) rn[kw] = __ldg(rbase + kw);
   }
+  if (UT > 0) {
+    static_assert(UT == 0 || (K33 && (UT == 1 || UT == 3)), "unit staging: 3x3 kernels, a row or a tap per unit");
+    const int nunits = a.cin * (9 / (UT > 0 ? UT : 1));
+    // one staged unit: refill the other buffer, wait for this one, its taps, barrier
+    auto unit = [&](int k, const uint32_t* rc) {
+      if (threadIdx.x == 0 && k + 1 < nunits) {
+        // buffer (k+1)&1 was last read in unit k-1, which ended with a CTA barrier
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(k + 1);
+      }
+      mbar_wait(&full[k & 1], (uint32_t)(k >> 1) & 1u);
+      const uint32_t* __restrict__ tb = smem_tab + (k & 1) * UBLK;
+#pragma unroll
+      for (int t = 0; t < UT; t++) smem_tap<F>(acc, rc[t], tb + t * R * S, a);
+      __syncthreads();  // buffer k&1 is refilled at unit k+2's issue
+    };
 #pragma unroll 1
-  for (int k = 0; k < nchunks; k++) {
+    for (int c = 0; c < a.cin; c++) {
+      const uint32_t* __restrict__ rc_base = rbase + c * cstride;
+#pragma unroll
+      for (int kh = 0; kh < 3; kh++) {
+        uint32_t rc[3];
+#pragma unroll
+        for (int kw = 0; kw < 3; kw++) rc[kw] = rn[kw];
+        if (kh < 2 || c + 1 < a.cin) {
+          const uint32_t* nrow = kh < 2 ? rc_base + (kh + 1) * Wp : rc_base + cstride;
+#pragma unroll
+          for (int kw = 0; kw < 3; kw++) rn[kw] = __ldg(nrow + kw);
+        }
+        if (UT == 3) {
+          unit(3 * c + kh, rc);
+        } else {
+#pragma unroll
+          for (int kw = 0; kw < 3; kw++) unit(9 * c + 3 * kh + kw, rc + kw);
+        }
+      }
+    }
+  }
+#pragma unroll 1
+  for (int k = 0; k < (UT > 0 ? 0 : nchunks); k++) {
     if (threadIdx.x == 0 && k + 1 < nchunks) {
       // buffer (k+1)&1 was last read in chunk k-1, which ended with a CTA barrier
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -659,16 +707,48 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const int64_t blk_bytes = (int64_t)tab_block_words<F>(a.kh * a.kw) * 4;
   const bool k33 = k3 && a.kh == 3;
   const bool smem_ok = 2 * blk_bytes <= 50 * 1024;
+  // unit staging (variant 8, 3x3, wF >= 6): a kernel row per buffer when the pair
+  // fits 64 KB (wF = 6, 7), else one tap per buffer (pair <= 100 KB: wF = 8, 9)
+  const int64_t row_bytes = blk_bytes / 3, tap_bytes = blk_bytes / 9;
+  const int ut = 2 * row_bytes <= 64 * 1024 ? 3 : (2 * tap_bytes <= 100 * 1024 ? 1 : 0);
+  const bool units_ok = k33 && F::WF >= 6 && F::WF <= 9 && ut > 0;
   if (variant == 0) {
     // auto: with fewer warps than 2 per SMSP the reduction chains are latency-bound:
     // one-warp CTAs (so every SM gets work) running the software-pipelined kernel;
-    // otherwise the tables staged in shared memory when a channel block pair fits
-    // (wF <= 5 for 3x3), else the L1-served kernels: prefetching one tap ahead when
-    // the table rows do not stay L1 resident (wF >= 6, measured on C5), or three kernel rows per
-    // unrolled loop body at <= 64 registers.
-    variant = warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : (F::WF >= 6 ? 4 : (k3 ? 6 : 3));
+    // otherwise the tables staged in shared memory -- a channel block per buffer when
+    // the pair fits (wF <= 5 for 3x3), a kernel row or a tap (wF = 6-9, 3x3) --, else
+    // the L1-served kernels: prefetching one tap ahead when the table rows do not stay
+    // L1 resident (wF >= 6, measured on C5), or three kernel rows per unrolled loop
+    // body at <= 64 registers.
+    variant = warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : units_ok ? 8 : (F::WF >= 6 ? 4 : (k3 ? 6 : 3));
   }
+  if (variant == 8 && !units_ok) variant = 7;
   if (variant == 7 && !smem_ok) variant = 6;
+  if (variant == 8) {
+    if constexpr (F::WF >= 6 && F::WF <= 9) {
+      const int64_t ub = ut == 3 ? row_bytes : tap_bytes;
+      auto go = [&](auto kern) {
+        static bool attr = false;  // once per kernel instantiation: allow up to 200 KB of dynamic smem
+        if (!attr) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          attr = true;
+        }
+        kern<<<grid(256), 256, (size_t)(2 * ub), s>>>(a);
+      };
+      // 256-thread CTAs, 4 per SM when their buffer pairs fit (measured on C5: 512-thread
+      // CTAs and per-channel staging at 2 CTAs / SM are slower)
+      // (HOBF_SMEM_CFG = 3: at most 3 per SM, 80 registers)
+      const bool four = a.smem_cfg != 3 && 8 * ub <= 216 * 1024, three = 6 * ub <= 216 * 1024;
+      if (ut == 3) {
+        if (four) go(conv_tab_smem_kernel<F, 256, 4, 1, true, 3>);
+        else go(conv_tab_smem_kernel<F, 256, 3, 1, true, 3>);
+      } else {
+        if (three) go(conv_tab_smem_kernel<F, 256, 3, 1, true, 1>);  // (4 per SM: spills, slower)
+        else go(conv_tab_smem_kernel<F, 256, 2, 1, true, 1>);
+      }
+    }
+    return cudaGetLastError();
+  }
   if (variant == 7) {
     const int sm = a.smem_cfg;  // development override (HOBF_SMEM_CFG): 0 auto, 2 or 3
     // >= 8 warps per SMSP of work: 128-thread CTAs x 8 per SM (one channel block per

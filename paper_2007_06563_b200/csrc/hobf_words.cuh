@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t requant_word(uint32_t x, int we, int wfi, in
 // everything one output-channel group needs for one input channel is one
 // contiguous block (one bulk copy).
 __host__ __device__ constexpr int tab_stride(int npt, int wf) {
-  return (wf > 5 || ((npt / 4) & 1)) ? npt : npt + 4;
+  return (wf > 7 || ((npt / 4) & 1)) ? npt : npt + 4;
 }
 
 }  // namespace hobf

@@ -268,8 +268,9 @@ def test_conv_prepared_full_vs_oracle(we, wf):
             assert np.array_equal(got, gpu_conv(x, w, f, relu=relu, prepared=False))
 
 
-@pytest.mark.parametrize("variant", [3, 4, 5, 6, 7])
-@pytest.mark.parametrize("we,wf,kh,kw", [(5, 3, 3, 3), (4, 6, 2, 3), (5, 10, 3, 3), (6, 2, 3, 2)])
+@pytest.mark.parametrize("variant", [3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("we,wf,kh,kw", [(5, 3, 3, 3), (4, 6, 2, 3), (5, 10, 3, 3), (6, 2, 3, 2), (4, 6, 3, 3),
+                                         (5, 7, 3, 3), (5, 8, 3, 3), (6, 9, 3, 3)])
 def test_conv_prepared_every_schedule(variant, we, wf, kh, kw):
     """Every kernel schedule of hobf_conv2d_prepared_variant gives the oracle's words:
     several 128-pixel CTAs with a ragged tail, a ragged last Cout group, cin not a
