@@ -735,26 +735,21 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
         }
         kern<<<grid(256), 256, (size_t)(2 * ub), s>>>(a);
       };
-      // 256-thread CTAs, 4 per SM when their buffer pairs fit (measured on C5: 512-thread
-      // CTAs and per-channel staging at 2 CTAs / SM are slower)
-      // (HOBF_SMEM_CFG = 3: at most 3 per SM, 80 registers)
-      const bool four = a.smem_cfg != 3 && 8 * ub <= 216 * 1024, three = 6 * ub <= 216 * 1024;
-      if (ut == 3) {
-        if (four) go(conv_tab_smem_kernel<F, 256, 4, 1, true, 3>);
-        else go(conv_tab_smem_kernel<F, 256, 3, 1, true, 3>);
-      } else {
-        if (three) go(conv_tab_smem_kernel<F, 256, 3, 1, true, 1>);  // (4 per SM: spills, slower)
-        else go(conv_tab_smem_kernel<F, 256, 2, 1, true, 1>);
-      }
+      // 256-thread CTAs, 3 per SM (80 registers; measured on C5: 4 per SM at 64
+      // registers, 512-thread CTAs and per-channel staging at 2 CTAs / SM are slower)
+      if (ut == 3) go(conv_tab_smem_kernel<F, 256, 3, 1, true, 3>);
+      else if (6 * ub <= 216 * 1024) go(conv_tab_smem_kernel<F, 256, 3, 1, true, 1>);
+      else go(conv_tab_smem_kernel<F, 256, 2, 1, true, 1>);
     }
     return cudaGetLastError();
   }
   if (variant == 7) {
-    const int sm = a.smem_cfg;  // development override (HOBF_SMEM_CFG): 0 auto, 2 or 3
-    // >= 8 warps per SMSP of work: 128-thread CTAs x 8 per SM (one channel block per
-    // buffer) when 8 x 2 blocks fit the SM's shared memory; otherwise (fewer warps, or
-    // larger blocks) 256-thread CTAs x 4 per SM (measured on C3 / C4 / C5)
-    const int cfg = sm ? sm : ((warps >= 148 * 4 * 8 && 16 * blk_bytes <= 216 * 1024) ? 2 : 3);
+    const int sm = a.smem_cfg;  // development override (HOBF_SMEM_CFG): 0 auto, 2, 3, 6 or 7
+    // 3x3 with >= 8 warps per SMSP of work: 128-thread CTAs x 6 per SM at <= 80
+    // registers (C3 0.846 / C4 0.887 of the roof, vs 0.827 / 0.869 at 8 x 64 registers);
+    // fewer warps (single partial wave): 256-thread CTAs x 3 (MOB 0.785 vs 0.767, C5
+    // +1%); measured, DESIGN.md section 6
+    const int cfg = sm ? sm : (warps >= 148 * 4 * 8 && 12 * blk_bytes <= 216 * 1024) ? 6 : 7;
     auto go = [&](auto kern, int nt, int cc) {
       static bool attr = false;  // once per kernel instantiation: allow up to 200 KB of dynamic smem
       if (!attr) {
@@ -764,8 +759,10 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
       kern<<<grid(nt), nt, (size_t)(2 * cc * blk_bytes), s>>>(a);
     };
     if (k33) {
-      if (cfg == 2) go(conv_tab_smem_kernel<F, 128, 8, 1, true>, 128, 1);
-      else go(conv_tab_smem_kernel<F, 256, 4, 1, true>, 256, 1);
+      if (cfg == 6) go(conv_tab_smem_kernel<F, 128, 6, 1, true>, 128, 1);
+      else if (cfg == 2) go(conv_tab_smem_kernel<F, 128, 8, 1, true>, 128, 1);
+      else if (cfg == 3) go(conv_tab_smem_kernel<F, 256, 4, 1, true>, 256, 1);
+      else go(conv_tab_smem_kernel<F, 256, 3, 1, true>, 256, 1);
     } else {
       go(conv_tab_smem_kernel<F, 256, 4, 1, false>, 256, 1);
     }
