@@ -736,6 +736,12 @@ static bool set_epilogue(ConvArgs& a, hobf_fmt f, hobf_epilogue ep, bool records
   return false;
 }
 
+// development overrides (HOBF_CONV_VARIANT, HOBF_SMEM_CFG)
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
                         const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
                         int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
@@ -766,6 +772,7 @@ hobf_status hobf_conv2d_ex(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
   a.variant = 0;
+  a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
   if (!set_epilogue(a, f, ep, false)) return HOBF_EINVAL;
   a.one = 1;
   a.two = 2u;
@@ -826,11 +833,6 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
   if (relu) *relu = e->g_relu;
   if (mac_tab) *mac_tab = e->g_tab;
   return HOBF_OK;
-}
-
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
 }
 
 // Kernel variant of hobf_conv2d_prepared (see launch_conv_tab); HOBF_CONV_VARIANT overrides.

@@ -686,8 +686,12 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   if (a.items == 0) return cudaSuccess;
   const int threads = 128;
   const int64_t blocks = (a.items + threads - 1) / threads;
-  if (a.kh == 3 && a.kw == 3)  // the channel's nine taps in one body, <= 80 registers
-    conv_direct_kernel<F, 6, true><<<(unsigned)blocks, threads, 0, s>>>(a);
+  // 3x3: the channel's nine taps in one body; CTAs per SM (register budget) by
+  // mantissa width, measured on C3's shape: wF <= 6 5 (<= 96 registers: e5m5 0.67 ->
+  // 0.70 of the roof vs 6), wF = 7, 8 6 (<= 80), wF >= 9 4 (<= 128: e5m10 0.60 -> 0.66)
+  constexpr int GM = F::WF >= 9 ? 4 : (F::WF >= 7 ? 6 : 5);
+  if (a.kh == 3 && a.kw == 3)
+    conv_direct_kernel<F, GM, true><<<(unsigned)blocks, threads, 0, s>>>(a);
   else
     conv_direct_kernel<F><<<(unsigned)blocks, threads, 0, s>>>(a);
   return cudaGetLastError();
