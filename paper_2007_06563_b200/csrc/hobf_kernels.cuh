@@ -777,7 +777,8 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   } else if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
     conv_tab_kernel<F, 32, 1, false, 3><<<grid(32), 32, 0, s>>>(a);
   } else if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
-    conv_tab_kernel<F, 128, 1, false, 1><<<grid(128), 128, 0, s>>>(a);
+    // <= 96 registers, 5 CTAs / SM (C3 e5m10 0.79 -> 0.81, C5 wF = 10 +0-3% vs 128 registers)
+    conv_tab_kernel<F, 128, 5, false, 1><<<grid(128), 128, 0, s>>>(a);
   } else if (k3) {     // kernel width 3 unrolled, <= 56 registers (9 CTAs / SM)
     conv_tab_kernel<F, 128, 9, true, 0><<<grid(128), 128, 0, s>>>(a);
   } else {
