@@ -60,14 +60,16 @@ def parse_args(argv=None):
     return ap.parse_args(argv)
 
 
-def measured_traffic(cfg_name, we, wf, use_tab):
-    """DRAM bytes per launch of the conv kernel from a committed ncu --set full capture, if any."""
+def measured_traffic(cfg_name, we, wf, use_tab, rtz=False, extended=False):
+    """DRAM bytes per launch of the conv kernel from a committed ncu capture of this exact
+    (config, format, rounding, MAC class, kernel), if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
             t = json.load(f)
     except (OSError, ValueError):
         return None
-    return t.get(f"{cfg_name}/e{we}m{wf}/{'conv2d_prepared' if use_tab else 'conv2d'}")
+    tag = f"e{we}m{wf}" + ("x" if extended else "") + ("_rtz" if rtz else "")
+    return t.get(f"{cfg_name}/{tag}/{'conv2d_prepared' if use_tab else 'conv2d'}")
 
 
 def fmt_of(cfg, override):
@@ -432,7 +434,7 @@ def run_gpu(a, dist):
                    "weight_prep_ms": weight_prep_ms,
                    "parallelism": f"dp{dist.world} (batch shards, no collective)"},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlop3/s",
-                     "frac": achieved / peak, "traffic": measured_traffic(cfg.name, we, wf, use_tab),
+                     "frac": achieved / peak, "traffic": measured_traffic(cfg.name, we, wf, use_tab, rnd == 1, bool(a.extended)),
                      "kernel": "conv2d_prepared (weight tables)" if use_tab else
                                "conv2d_dw (depthwise, full lop3 MAC)" if cfg.dw else "conv2d (full lop3 MAC)",
                      "gates_per_32lane_mac": G, "gates_full_mac": g["mac"],
