@@ -802,6 +802,7 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((c + 31) / 32);
   a.variant = 0;
+  a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
   if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;
   a.one = 1;
   a.two = 2u;
