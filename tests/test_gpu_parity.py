@@ -424,6 +424,29 @@ def test_conv_extended_class(we, wf, prepared):
         assert np.array_equal(got, exp), np.argwhere(got != exp)[:5]
 
 
+@pytest.mark.parametrize("variant", [4, 6, 7, 8])
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 6), (5, 7), (5, 8)])
+def test_conv_extended_every_schedule(variant, we, wf):
+    """Extended class through the explicit schedules (the auto schedule of the small
+    cases above is the latency-bound one): staged channel blocks, kernel rows, taps,
+    L1-served; ragged CTAs and Cout group, stride 1 and 2."""
+    H = hobf()
+    n, h, w, cin, cout, pad = 3, 11, 13, 5, 40, 1
+    x, wt = inputs.small_case(300 + 10 * we + wf, n, h, w, cin, cout, "normal", 0.4)
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd, extended=1)
+        for s_ in (1, 2):
+            exp = oracle_conv(x, wt, f, stride=s_, pad=pad, relu=0)
+            xp = H.quantize_pack(we, wf, torch.from_numpy(x.reshape(-1, cin)).cuda(), rnd)
+            wp = H.quantize_pack(we, wf, torch.from_numpy(wt.reshape(-1, cout)).cuda(), rnd)
+            tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
+            xr = H.prepare_activations(f, xp, n, h, w, cin, pad)
+            yp = H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, s_, pad, 0, variant=variant)
+            ho, wo = H.conv_out_hw(h, w, 3, 3, s_, pad)
+            got = to_np_words(H.unpack(we, f.wfo, yp, n * ho * wo, cout)).reshape(exp.shape)
+            assert np.array_equal(got, exp), (variant, rnd, s_, np.argwhere(got != exp)[:5])
+
+
 @pytest.mark.parametrize("we,wf", [(5, 3), (4, 7), (6, 10)])
 @pytest.mark.parametrize("rnd", [0, 1])
 def test_mac_random_extended(we, wf, rnd):
