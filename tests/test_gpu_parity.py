@@ -361,7 +361,7 @@ def test_conv_configs_sampled(name, prepared):
 def test_conv_C5_sweep_sampled():
     H = hobf()
     cfg = inputs.CONFIGS["C5"]
-    x, w = inputs.draw(cfg, n=8)  # batch prefix of the config's draw
+    x, w = inputs.draw(cfg)  # full batch: the bench's launch configuration (staged schedules 7 / 8)
     rng = np.random.default_rng(6)
     for (we, wf) in cfg.formats:
         f = H.Fmt(we, wf, 0)
