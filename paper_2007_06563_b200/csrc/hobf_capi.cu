@@ -593,7 +593,6 @@ __global__ void __launch_bounds__(256) build_wtab_kernel(const uint32_t* __restr
           out[u] = lane == j ? bal : out[u];
         }
       }
-#pragma unroll
       // weight row (tap, c) of group g -> table block [g][c][tap] (hobf_words.cuh);
       // the stride padding words stay zero
       const int64_t wrow = grp / G, g = grp % G;
