@@ -12,6 +12,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "hobf_internal.h"
 #include "hobf_words.cuh"
 
@@ -688,6 +692,19 @@ __global__ void __launch_bounds__(256) mac_planes_kernel(uint32_t* __restrict__ 
   }
 }
 
+// Opt a kernel in to up to 200 KB of dynamic shared memory, once per (kernel,
+// device): the attribute is per function and per device, so a process that
+// launches several instantiations or uses several GPUs sets each one.
+inline void allow_big_smem(const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({kern, dev}).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
 template <class F>
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   if (a.items == 0) return cudaSuccess;
@@ -739,11 +756,7 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     if constexpr (F::WF >= 6 && F::WF <= 9) {
       const int64_t ub = ut == 3 ? row_bytes : tap_bytes;
       auto go = [&](auto kern) {
-        static bool attr = false;  // once per kernel instantiation: allow up to 200 KB of dynamic smem
-        if (!attr) {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-          attr = true;
-        }
+        allow_big_smem((const void*)kern);
         kern<<<grid(256), 256, (size_t)(2 * ub), s>>>(a);
       };
       // 256-thread CTAs, 3 per SM (80 registers; measured on C5: 4 per SM at 64
@@ -762,11 +775,7 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     // +1%); measured, DESIGN.md section 6
     const int cfg = sm ? sm : (warps >= 148 * 4 * 8 && 12 * blk_bytes <= 216 * 1024) ? 6 : 7;
     auto go = [&](auto kern, int nt, int cc) {
-      static bool attr = false;  // once per kernel instantiation: allow up to 200 KB of dynamic smem
-      if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
+      allow_big_smem((const void*)kern);
       kern<<<grid(nt), nt, (size_t)(2 * cc * blk_bytes), s>>>(a);
     };
     if (k33) {

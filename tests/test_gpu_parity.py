@@ -447,6 +447,28 @@ def test_conv_extended_every_schedule(variant, we, wf):
             assert np.array_equal(got, exp), (variant, rnd, s_, np.argwhere(got != exp)[:5])
 
 
+def test_staged_launch_shapes_same_format():
+    """One format through both launch shapes of the staged schedule in one process
+    (256 x 3 for a partial wave, then 128 x 6 for >= 8 warps per SMSP): each kernel
+    instantiation needs its own > 48 KB shared-memory opt-in (a 49 KB table pair)."""
+    H = hobf()
+    f = H.Fmt(4, 5, 1, extended=1)
+    rng = np.random.default_rng(17)
+    for n, h, w, cin, cout in [(2, 11, 13, 3, 40), (26, 56, 56, 2, 64)]:
+        x, wt = inputs.small_case(400 + n, n, h, w, cin, cout, "normal", 0.5)
+        xp = H.quantize_pack(4, 5, torch.from_numpy(x.reshape(-1, cin)).cuda(), 1)
+        wp = H.quantize_pack(4, 5, torch.from_numpy(wt.reshape(-1, cout)).cuda(), 1)
+        tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
+        xr = H.prepare_activations(f, xp, n, h, w, cin, 1)
+        yp = H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, 0, variant=7)
+        got = to_np_words(H.unpack(4, f.wfo, yp, n * h * w, cout))
+        idx = rng.integers(0, got.size, 400)
+        xq = oracle.encode_f32(x, 4, 5, 1)
+        wq = oracle.encode_f32(wt, 4, 5, 1)
+        exp = oracle.conv2d_sample(xq, wq, idx, 4, 5, f.wfo, 1)
+        assert np.array_equal(got.ravel()[idx], exp), (n, h, w)
+
+
 @pytest.mark.parametrize("we,wf", [(5, 3), (4, 7), (6, 10)])
 @pytest.mark.parametrize("rnd", [0, 1])
 def test_mac_random_extended(we, wf, rnd):
