@@ -538,7 +538,7 @@ __device__ __forceinline__ void smem_tap(uint32_t* acc, uint32_t rec, const uint
 // channel blocks); K33: kh = kw = 3, the channel's nine taps fully unrolled.
 // UT > 0 (K33 only): UT taps of one channel per staged buffer -- 3 = one kernel
 // row, 1 = one tap -- for the formats whose channel block pair does not fit
-// (wF >= 6): the flat unit k = (9 c + 3 kh + kw) / UT is the contiguous slice
+// (wF >= 6; wF = 5 of the extended class): the flat unit k = (9 c + 3 kh + kw) / UT is the contiguous slice
 // of UT taps of the group's block.
 template <class F, int NT, int MINB, int CC, bool K33, int UT = 0>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
@@ -735,11 +735,11 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const int64_t blk_bytes = (int64_t)tab_block_words<F>(a.kh * a.kw) * 4;
   const bool k33 = k3 && a.kh == 3;
   const bool smem_ok = 2 * blk_bytes <= 50 * 1024;
-  // unit staging (variant 8, 3x3, wF >= 6): a kernel row per buffer when the pair
+  // unit staging (variant 8, 3x3, wF >= 6, or 5 extended): a kernel row per buffer when the pair
   // fits 64 KB (wF = 6, 7), else one tap per buffer (pair <= 100 KB: wF = 8, 9)
   const int64_t row_bytes = blk_bytes / 3, tap_bytes = blk_bytes / 9;
   const int ut = 2 * row_bytes <= 64 * 1024 ? 3 : (2 * tap_bytes <= 100 * 1024 ? 1 : 0);
-  const bool units_ok = k33 && F::WF >= 6 && F::WF <= 9 && ut > 0;
+  const bool units_ok = k33 && F::WF >= 5 && F::WF <= 9 && ut > 0;  // (wF = 5: extended class)
   if (variant == 0) {
     // auto: with fewer warps than 2 per SMSP the reduction chains are latency-bound:
     // one-warp CTAs (so every SM gets work) running the software-pipelined kernel;
@@ -753,7 +753,7 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   if (variant == 8 && !units_ok) variant = 7;
   if (variant == 7 && !smem_ok) variant = 6;
   if (variant == 8) {
-    if constexpr (F::WF >= 6 && F::WF <= 9) {
+    if constexpr (F::WF >= 5 && F::WF <= 9) {
       const int64_t ub = ut == 3 ? row_bytes : tap_bytes;
       auto go = [&](auto kern) {
         allow_big_smem((const void*)kern);
@@ -793,8 +793,10 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   } else if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
     conv_tab_kernel<F, 32, 1, false, 3><<<grid(32), 32, 0, s>>>(a);
   } else if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
-    // <= 96 registers, 5 CTAs / SM (C3 e5m10 0.79 -> 0.81, C5 wF = 10 +0-3% vs 128 registers)
-    conv_tab_kernel<F, 128, 5, false, 1><<<grid(128), 128, 0, s>>>(a);
+    // <= 96 registers, 5 CTAs / SM (C3 e5m10 0.79 -> 0.81, C5 wF = 10 +0-3% vs 128 registers);
+    // the extended class's largest circuits (> 400 lop3) get 128 (4 CTAs / SM)
+    constexpr int M4 = F::G_TAB > 400 ? 4 : 5;
+    conv_tab_kernel<F, 128, M4, false, 1><<<grid(128), 128, 0, s>>>(a);
   } else if (k3) {     // kernel width 3 unrolled, <= 56 registers (9 CTAs / SM)
     conv_tab_kernel<F, 128, 9, true, 0><<<grid(128), 128, 0, s>>>(a);
   } else {
