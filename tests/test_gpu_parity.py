@@ -425,7 +425,7 @@ def test_conv_extended_class(we, wf, prepared):
 
 
 @pytest.mark.parametrize("variant", [4, 6, 7, 8])
-@pytest.mark.parametrize("we,wf", [(5, 3), (4, 6), (5, 7), (5, 8)])
+@pytest.mark.parametrize("we,wf", [(5, 3), (6, 5), (4, 6), (5, 7), (5, 8), (5, 9)])
 def test_conv_extended_every_schedule(variant, we, wf):
     """Extended class through the explicit schedules (the auto schedule of the small
     cases above is the latency-bound one): staged channel blocks, kernel rows, taps,
