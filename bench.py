@@ -179,8 +179,10 @@ def run_reference(a, dist):
     x, w = inputs.draw(cfg, n=1)
     per_img = cfg.macs(1)
     # bounded sample per step: the conv of the first `rows` input rows of image 0
-    # (an image of height `rows`), sized so that K+W steps take a few minutes
-    rows = max(1, min(cfg.h, int(round(cfg.h * min(1.0, 0.4e9 / per_img)))))
+    # (an image of height `rows`), sized so that K+W steps take a few minutes at
+    # the oracle's ~0.3e9 MAC/s: at most 0.4e9 MACs a step, 3.6e10 in all
+    budget = min(0.4e9, 3.6e10 / max(1, a.steps + a.warmup))
+    rows = max(1, min(cfg.h, int(round(cfg.h * min(1.0, budget / per_img)))))
     xq = oracle.encode_f32(x, we, wf, rnd)
     wq = oracle.encode_f32(w, we, wf, rnd)
     xin = np.ascontiguousarray(xq[:, :rows])
