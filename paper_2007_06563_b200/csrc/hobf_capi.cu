@@ -473,11 +473,16 @@ __global__ void __launch_bounds__(256) quantize_acts_kernel(const float* __restr
                                                             uint32_t* __restrict__ rec) {
   __shared__ uint32_t tile[32][33];
   const int Hp = h + 2 * pad, Wp = w + 2 * pad;
-  const int xb = blockIdx.x * 32;          // first padded column of the tile
-  const int cb = blockIdx.y * 32;          // first channel of the tile
-  const int ni = blockIdx.z / Hp, iyp = blockIdx.z % Hp;
-  const int iy = iyp - pad;
+  const int xtiles = (Wp + 31) / 32, ctiles = (cin + 31) / 32;
+  const int64_t ntiles = (int64_t)n * Hp * xtiles * ctiles;
   const uint32_t zero_rec = xrec_of(0u, we, wf);
+  // flattened tiles (column tile fastest), grid-stride: no grid dimension limit
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const int xb = (int)(t % xtiles) * 32;   // first padded column of the tile
+  const int cb = (int)((t / xtiles) % ctiles) * 32;  // first channel of the tile
+  const int64_t rowi = t / ((int64_t)xtiles * ctiles);
+  const int ni = (int)(rowi / Hp), iyp = (int)(rowi % Hp);
+  const int iy = iyp - pad;
   // all of this thread's loads first (4 in flight per thread), then the encodes
   constexpr int K = 32 / 8;  // blockDim.y == 8
   float xv[K];
@@ -499,6 +504,8 @@ __global__ void __launch_bounds__(256) quantize_acts_kernel(const float* __restr
     const int c = cb + k, ixp = xb + threadIdx.x;
     if (c < cin && ixp < Wp) rec[(((int64_t)ni * cin + c) * Hp + iyp) * Wp + ixp] = tile[threadIdx.x][k];
   }
+  __syncthreads();  // the tile is refilled by the next iteration
+  }
 }
 
 // Row-wise variant (the fast path when cin % 4 == 0 and x is 16-byte aligned):
@@ -508,15 +515,15 @@ __global__ void __launch_bounds__(256) quantize_acts_kernel(const float* __restr
 // the records transposed into shared memory [c][stride]; phase 2 writes each
 // channel's padded record row (Wp words, contiguous in the [n][c][Hp][Wp]
 // layout) with coalesced stores, padding columns / rows as +0 records.
-__global__ void __launch_bounds__(256) quantize_acts_row_kernel(const float* __restrict__ x, int n, int h, int w,
-                                                                int cin, int pad, int we, int wf, int rnd, int cc,
-                                                                int stride, uint32_t* __restrict__ rec) {
-  extern __shared__ uint32_t srec[];  // [cc][stride], stride odd
+// One (image ni, padded row iyp, channel chunk c0) tile; srec = [cc][stride].
+__device__ __forceinline__ void quantize_row_tile(const float* __restrict__ x, int n, int h, int w, int cin, int pad,
+                                                  int we, int wf, int rnd, int cc, int stride,
+                                                  uint32_t* __restrict__ rec, uint32_t* srec, int iyp, int ni,
+                                                  int c0) {
   const int Hp = h + 2 * pad, Wp = w + 2 * pad;
-  const int iyp = blockIdx.x, ni = blockIdx.y, c0 = blockIdx.z * cc;
+  const uint32_t zero_rec = xrec_of(0u, we, wf);
   const int ncc = min(cc, cin - c0);
   const int iy = iyp - pad;
-  const uint32_t zero_rec = xrec_of(0u, we, wf);
   if (iy >= 0 && iy < h) {
     // thread -> (pixel lane, channel quad) once; no division in the loops
     const int quads = ncc >> 2;
@@ -552,6 +559,32 @@ __global__ void __launch_bounds__(256) quantize_acts_row_kernel(const float* __r
       const int ix = ixp - pad;
       drow[ixp] = (row_in && ix >= 0 && ix < w) ? srow[ix] : zero_rec;
     }
+  }
+}
+
+__global__ void __launch_bounds__(256) quantize_acts_row_kernel(const float* __restrict__ x, int n, int h, int w,
+                                                                int cin, int pad, int we, int wf, int rnd, int cc,
+                                                                int stride, uint32_t* __restrict__ rec) {
+  extern __shared__ uint32_t srec[];  // [cc][stride], stride odd
+  quantize_row_tile(x, n, h, w, cin, pad, we, wf, rnd, cc, stride, rec, srec, blockIdx.x, blockIdx.y,
+                    blockIdx.z * cc);
+}
+
+// Same tiles flattened (padded row fastest) with a grid-stride loop, for shapes
+// past the grid's y / z limits (n or channel chunks > 65535).
+__global__ void __launch_bounds__(256) quantize_acts_row_flat_kernel(const float* __restrict__ x, int n, int h,
+                                                                     int w, int cin, int pad, int we, int wf,
+                                                                     int rnd, int cc, int stride,
+                                                                     uint32_t* __restrict__ rec) {
+  extern __shared__ uint32_t srec[];
+  const int Hp = h + 2 * pad;
+  const int chunks = (cin + cc - 1) / cc;
+  const uint64_t ntiles = (uint64_t)n * Hp * chunks;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t rest = t / Hp;
+    quantize_row_tile(x, n, h, w, cin, pad, we, wf, rnd, cc, stride, rec, srec, (int)(t % Hp), (int)(rest % n),
+                      (int)(rest / n) * cc);
+    __syncthreads();  // srec is refilled by the next tile
   }
 }
 
@@ -912,14 +945,23 @@ hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, i
   const int stride = w | 1;  // odd smem row stride: the transposed writes spread over the banks
   const int cc = (int)std::min<int64_t>(std::min<int64_t>(cin, 256),
                                         std::max<int64_t>(4, (32 * 1024 / 4) / stride) / 4 * 4);
-  if ((cin & 3) == 0 && aligned16(d_x) && n <= 65535 && Hp <= 2147483647) {
-    dim3 grid((unsigned)Hp, (unsigned)n, (unsigned)((cin + cc - 1) / cc));
-    quantize_acts_row_kernel<<<grid, 256, (size_t)cc * stride * 4, (cudaStream_t)stream>>>(
-        d_x, n, h, w, cin, pad, f.we, f.wf, f.round, cc, stride, d_xrec);
+  const int64_t kMaxGrid = 2147483647LL;
+  if ((cin & 3) == 0 && aligned16(d_x)) {
+    const int chunks = (cin + cc - 1) / cc;
+    const size_t smem = (size_t)cc * stride * 4;
+    if (n <= 65535 && chunks <= 65535) {
+      quantize_acts_row_kernel<<<dim3((unsigned)Hp, (unsigned)n, (unsigned)chunks), 256, smem,
+                                 (cudaStream_t)stream>>>(d_x, n, h, w, cin, pad, f.we, f.wf, f.round, cc, stride,
+                                                         d_xrec);
+    } else {
+      const int64_t tiles = (int64_t)n * Hp * chunks;
+      quantize_acts_row_flat_kernel<<<(unsigned)std::min(tiles, kMaxGrid), 256, smem, (cudaStream_t)stream>>>(
+          d_x, n, h, w, cin, pad, f.we, f.wf, f.round, cc, stride, d_xrec);
+    }
   } else {
-    dim3 grid((unsigned)((Wp + 31) / 32), (unsigned)((cin + 31) / 32), (unsigned)(n * Hp));
-    quantize_acts_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(d_x, n, h, w, cin, pad, f.we, f.wf,
-                                                                        f.round, d_xrec);
+    const int64_t tiles = (int64_t)n * Hp * ((Wp + 31) / 32) * ((cin + 31) / 32);
+    quantize_acts_kernel<<<(unsigned)std::min(tiles, kMaxGrid), dim3(32, 8), 0, (cudaStream_t)stream>>>(
+        d_x, n, h, w, cin, pad, f.we, f.wf, f.round, d_xrec);
   }
   if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
   g_last_launches = 1;
@@ -948,6 +990,7 @@ hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t 
   if (h == 0 || w == 0 || cin == 0 || kh == 0 || kw == 0 || cout == 0) return HOBF_ESHAPE;
   const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
   if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
+  if ((cout + 31) / 32 > 65535) return HOBF_ESHAPE;  // output-channel groups index grid.y
   const FormatEntry* e = tab_format(f);
   if (!e) return HOBF_EUNSUPPORTED;
   if (n == 0) return HOBF_OK;

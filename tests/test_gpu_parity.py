@@ -252,6 +252,35 @@ def test_conv_C1_full():
             assert np.array_equal(got, exp), (rnd, relu, np.argwhere(got != exp)[:5])
 
 
+def test_conv_prepared_int64_indexing():
+    """Maximum-size case: 7.5 M 1x1 images x 32 channels, so the zero-padded record
+    buffer holds 2.16e9 words (indices past 2^31) and the output planes 9e7 words;
+    the bench's launch shape (TMA-staged tables, 128 x 6 CTAs/SM).  Sampled outputs
+    (the last images included) vs the oracle.  ~12 GB of device memory."""
+    H = hobf()
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40e9:
+        pytest.skip("needs ~12 GB of free device memory (+ headroom)")
+    n, h, w, cin, cout = 7_500_000, 1, 1, 32, 32
+    f = H.Fmt(5, 3, 0)
+    x, wt = inputs.small_case(511, n, h, w, cin, cout, "relu_normal", 0.2)
+    assert n * cin * 3 * 3 > 2 ** 31
+    xt = torch.from_numpy(x).cuda()
+    wp = H.quantize_pack(5, 3, torch.from_numpy(wt.reshape(-1, cout)).cuda(), 0)
+    tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
+    xr = H.quantize_activations(f, xt, 1)
+    del xt
+    yp = H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, 0)
+    del xr
+    got = to_np_words(H.unpack(5, f.wfo, yp, n * h * w, cout)).ravel()
+    rng = np.random.default_rng(7)
+    idx = np.unique(np.concatenate([rng.integers(0, got.size, 300), np.arange(got.size - 96, got.size)]))
+    xq = oracle.encode_f32(x, 5, 3, 0)
+    wq = oracle.encode_f32(wt, 5, 3, 0)
+    exp = oracle.conv2d_sample(xq, wq, idx, 5, 3, f.wfo, 0)
+    assert np.array_equal(got[idx], exp)
+
+
 @pytest.mark.parametrize("we,wf", [(5, 3), (4, 3), (6, 2), (4, 7)])
 def test_conv_prepared_full_vs_oracle(we, wf):
     """The weight-table path in full on a C1-shaped layer with every special class present."""
@@ -406,6 +435,21 @@ def test_activation_records_two_ways_agree(we, wf, pad):
         if pad:
             assert np.all(rec[:, :, 0, :] == np.uint32((1 << wf) << 20))
 
+
+
+@pytest.mark.parametrize("n,h,w,cin", [(70_000, 1, 1, 8), (70_000, 1, 2, 5)])
+def test_activation_records_many_images(n, h, w, cin):
+    """More images than a grid's y / z dimension holds (65535): the flattened-tile
+    quantise kernels (row kernel for cin % 4 == 0, tile-transpose kernel otherwise)."""
+    H = hobf()
+    rng = np.random.default_rng(n + cin)
+    x = rng.standard_normal((n, h, w, cin)).astype(np.float32)
+    f = H.Fmt(5, 3, 0)
+    pad = 1
+    rec = to_np_words(H.quantize_activations(f, torch.from_numpy(x).cuda(), pad)).reshape(n, cin, h + 2, w + 2)
+    inner = rec[:, :, pad:pad + h, pad:pad + w] & np.uint32((1 << 20) - 1)
+    assert np.array_equal(inner.transpose(0, 2, 3, 1), oracle.encode_f32(x, 5, 3, 0))
+    assert np.all(rec[:, :, 0, :] == np.uint32((1 << 3) << 20))
 
 
 # ----------------------------------------------------------------------------- extended class (P:151-177, P:262)
