@@ -30,7 +30,9 @@
  *     The library keeps no device allocation and no mutable global state.
  *   - Argument checks are synchronous and return HOBF_EINVAL (null pointer,
  *     negative size, misaligned pointer, format out of range) / HOBF_ESHAPE
- *     (inconsistent shapes) / HOBF_EUNSUPPORTED (no generated kernel for the
+ *     (inconsistent shapes; a conv with more than 65535 x 32 output channels or
+ *     more than (2^31 - 1) x 32 (pixel, 32-channel group) items -- the launch
+ *     grid's limits) / HOBF_EUNSUPPORTED (no generated kernel for the
  *     format) before anything is launched.  Work is enqueued asynchronously on
  *     `stream` (a cudaStream_t; NULL = legacy default stream); a launch failure
  *     returns HOBF_ECUDA.  Nothing aborts or throws across the ABI.

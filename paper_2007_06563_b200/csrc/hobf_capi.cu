@@ -768,6 +768,10 @@ static bool set_epilogue(ConvArgs& a, hobf_fmt f, hobf_epilogue ep, bool records
   return false;
 }
 
+// largest (pixel, output-channel group) count a conv launch covers: grid.x < 2^31
+// blocks of >= 32 threads
+static const int64_t kMaxConvItems = 2147483647LL * 32;
+
 // development overrides (HOBF_CONV_VARIANT, HOBF_SMEM_CFG)
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -803,6 +807,7 @@ hobf_status hobf_conv2d_ex(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
   a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
+  if (a.items > kMaxConvItems) return HOBF_ESHAPE;  // one grid.x block per <= 32 items
   a.variant = 0;
   a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
   if (!set_epilogue(a, f, ep, false)) return HOBF_EINVAL;
@@ -833,6 +838,7 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
   a.n = n; a.h = h; a.w = w; a.cin = c; a.kh = kh; a.kw = kw; a.cout = c;
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((c + 31) / 32);
+  if (a.items > kMaxConvItems) return HOBF_ESHAPE;  // one grid.x block per <= 32 items
   a.variant = 0;
   a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
   if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;
@@ -1001,6 +1007,7 @@ hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t 
   a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
   a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
   a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
+  if (a.items > kMaxConvItems) return HOBF_ESHAPE;  // one grid.x block per <= 32 items
   a.variant = variant;
   a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
   if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;

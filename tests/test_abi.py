@@ -78,6 +78,12 @@ def test_argument_errors_are_synchronous_and_need_no_gpu():
     assert lib.hobf_conv2d_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(hobf.OUT_NEXT_RECORDS, 3, 1), P, None) == 1
     assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(0, 0, 0), P, 9, None) == 1
     assert lib.hobf_conv2d_dw(f, P, 1, 2, 2, 8, P, 5, 5, 1, 0, 0, E(0, 0, 0), P, None) == 2
+    # beyond the launch grid's limits -> ESHAPE (not a launch failure)
+    big = 2 ** 31 - 1
+    assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 65536 * 32, 1, 1, 0, E(0, 0, 0), P, 0, None) == 2
+    assert lib.hobf_conv2d_prepared_ex(f, P, big, 4096, 4096, 4, P, 3, 3, 32, 1, 1, 0, E(0, 0, 0), P, 0, None) == 2
+    assert lib.hobf_conv2d_ex(f, P, big, 4096, 4096, 4, P, 3, 3, 32, 1, 1, 0, E(0, 0, 0), P, None) == 2
+    assert lib.hobf_conv2d_dw(f, P, big, 4096, 4096, 32, P, 3, 3, 1, 1, 0, E(0, 0, 0), P, None) == 2
 
 
 def test_binding_fails_loudly_without_library(tmp_path):
