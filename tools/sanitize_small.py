@@ -25,7 +25,7 @@ for f in (H.Fmt(5, 3, 0), H.Fmt(5, 10, 1), H.Fmt(4, 3, 0, extended=1)):
     if H.wtab_words(f, 3, 3, cin, cout) > 0:
         tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
         xr = H.quantize_activations(f, xt, 1)
-        for v in (3, 4, 5, 6, 7):
+        for v in (3, 4, 5, 6, 7, 8):
             y2 = H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, 1, variant=v)
             assert torch.equal(y1, y2), v
         r = H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, 1, nxt=H.Next(3, records=True, pad=1))
