@@ -162,7 +162,19 @@ uint32_t ref_add(uint32_t a, uint32_t b, int we, int wf, int mode) {
         return enc_special(CLS_ZERO, x.sign & y.sign, we, wf);
     if (x.cls == CLS_ZERO) return round_to(y.sign, y.M, y.e, we, wf, mode); /* exact: 0 + y = y */
     if (y.cls == CLS_ZERO) return round_to(x.sign, x.M, x.e, we, wf, mode); /* exact: x + 0 = x */
-    /* normal + normal: exact sum over the common exponent min(ex, ey) */
+    /* normal + normal.  Far-apart operands first: let X be the operand with the
+     * larger exponent (X = Mx 2^ex, Mx in [2^wf, 2^(wf+1))) and d = ex - ey.  If
+     * d >= wf + 3 then 0 < |Y| < 2^(ey+wf+1) <= 2^(ex-2), so the exact sum lies
+     * strictly between X and X +- 2^(ex-2), an open interval that holds no point
+     * of the F(wE, wf) grid and no RNE midpoint (the grid spacing is 2^ex at X's
+     * binade and 2^(ex-1) in the binade below).  Every rounding decision is then
+     * fixed by X and the sign of Y alone, so Y may be replaced by any value of the
+     * same sign in that interval -- here (-1)^sy 2^(ex-3) -- without changing the
+     * result.  This keeps the alignment shift below wf + 3 bits (exponent gaps
+     * reach 2^wE - 1 + wf, beyond the 128-bit integer for wE >= 7). */
+    if (x.e - y.e >= wf + 3) { y.M = 1; y.e = x.e - 3; }
+    else if (y.e - x.e >= wf + 3) { x.M = 1; x.e = y.e - 3; }
+    /* exact sum over the common exponent min(ex, ey) */
     int e = x.e < y.e ? x.e : y.e;
     i128 sx = (i128)(x.M << (x.e - e));
     i128 sy = (i128)(y.M << (y.e - e));

@@ -206,6 +206,51 @@ def test_mul_add_random_wide_vs_float64(we, wf, mode):
     assert np.array_equal(got[sel], exp[sel])
 
 
+WIDE_EXP = [(7, 4), (7, 11), (8, 4), (8, 11)]
+
+
+@pytest.mark.parametrize("we,wf", WIDE_EXP)
+def test_add_mul_wide_exponent_vs_float64(we, wf):
+    """wE = 7, 8 (exponent gaps up to 2^wE - 1, past a 128-bit alignment shift):
+    10^6 random normal pairs, add and mul in RNE against float64 library rounding
+    (double rounding through 53 bits is innocuous for p = wF + 1 <= 12 since
+    53 >= 2p + 2; the float64 product is exact), plus every exponent gap around the
+    far-operand threshold wF + 3 of ref_add."""
+    rng = np.random.default_rng(40 + we * 100 + wf)
+    N = 1_000_000
+    A, B = random_normals(rng, N, we, wf), random_normals(rng, N, we, wf)
+    # a quarter of the pairs with exponent gap d in [0, wf + 6], both orders
+    q = N // 4
+    ea = (A[:q].astype(np.int64) >> wf) & ((1 << we) - 1)
+    d = rng.integers(0, wf + 7, q) * np.where(rng.random(q) < 0.5, 1, -1)
+    eb = np.clip(ea + d, 0, (1 << we) - 1)
+    B[:q] = ((B[:q].astype(np.int64) & ~(((1 << we) - 1) << wf)) | (eb << wf)).astype(np.uint32)
+    got = oracle.add(A, B, we, wf, 0)
+    exp, _ = libpin.add_normals(A, B, we, wf, 0)
+    bad = np.nonzero(got != exp)[0]
+    assert bad.size == 0, [(hex(A[i]), hex(B[i]), hex(got[i]), hex(exp[i])) for i in bad[:5]]
+    got = oracle.mul(A, B, we, wf, wf + 1, 0)
+    assert np.array_equal(got, libpin.mul_normals(A, B, we, wf, wf + 1, 0))
+
+
+@pytest.mark.parametrize("we,wf", WIDE_EXP)
+@pytest.mark.parametrize("mode", [0, 1])
+def test_add_wide_exponent_vs_rational(we, wf, mode):
+    """The same widths against the exact-rational reference in both modes (RTZ has
+    no float64 pin once the gap exceeds 53 - wF - 2 bits), gaps around wF + 3."""
+    rng = np.random.default_rng(50 + we * 100 + wf + mode)
+    N = 3000 if wf <= 4 else 400  # the grid search of pyref grows with 2^wF
+    A, B = random_normals(rng, N, we, wf), random_normals(rng, N, we, wf)
+    ea = (A.astype(np.int64) >> wf) & ((1 << we) - 1)
+    d = rng.integers(wf, wf + 6, N) * np.where(rng.random(N) < 0.5, 1, -1)
+    eb = np.where(np.arange(N) < N // 2, np.clip(ea + d, 0, (1 << we) - 1), (B.astype(np.int64) >> wf) & ((1 << we) - 1))
+    B = ((B.astype(np.int64) & ~(((1 << we) - 1) << wf)) | (eb << wf)).astype(np.uint32)
+    got = oracle.add(A, B, we, wf, mode)
+    exp = np.array([pyref.add(int(a), int(b), we, wf, mode) for a, b in zip(A, B)], np.uint32)
+    bad = np.nonzero(got != exp)[0]
+    assert bad.size == 0, [(hex(A[i]), hex(B[i]), hex(got[i]), hex(exp[i])) for i in bad[:5]]
+
+
 # ----------------------------------------------------------------------------- IEEE library coincidence
 
 def half_words_normal(h):
