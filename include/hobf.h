@@ -27,7 +27,10 @@
  *
  * CONVENTIONS
  *   - The caller owns every buffer; device pointers must be 16-byte aligned.
- *     The library keeps no device allocation and no mutable global state.
+ *     The library keeps no device allocation.  Its only mutable state is the
+ *     per-thread launch counter (hobf_last_launch_count) and a mutex-guarded
+ *     record of which kernels were already opted in to > 48 KB of dynamic
+ *     shared memory on which device; nothing reads the environment.
  *   - Argument checks are synchronous and return HOBF_EINVAL (null pointer,
  *     negative size, misaligned pointer, format out of range) / HOBF_ESHAPE
  *     (inconsistent shapes; a conv with more than 65535 x 32 output channels or
@@ -181,9 +184,21 @@ hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, 
  *                          +0 record of F(we, next_wf) is (2^next_wf) << 20).
  *                          Needs 3+we+next_wf <= 20 and next_wf <= 10
  *                          (hobf_conv2d_prepared_ex only).
- * next_wf / next_pad are ignored for HOBF_OUT_PLANES; inconsistent values ->
- * HOBF_EINVAL.  The oracle's definition is ref_convert(relu(acc)). */
-typedef enum { HOBF_OUT_PLANES = 0, HOBF_OUT_NEXT_PLANES = 1, HOBF_OUT_NEXT_RECORDS = 2 } hobf_out_mode;
+ *   HOBF_OUT_F32           the last layer (floats only at the network's
+ *                          edges): every output word of F(we, wfo) decoded to
+ *                          its exact float32 value ((-1)^s 1.f 2^(E-bias); +-0,
+ *                          +-inf, NaN = 0x7FC00000), written NHWC as float
+ *                          [n][ho][wo][cout] (d_out is a float*, 16-byte
+ *                          aligned) -- what hobf_unpack_f32 of the planes
+ *                          gives, without the planes.  Needs we <= 7.
+ * next_wf / next_pad are ignored for HOBF_OUT_PLANES / HOBF_OUT_F32; inconsistent
+ * values -> HOBF_EINVAL.  The oracle's definition is ref_convert(relu(acc)). */
+typedef enum {
+  HOBF_OUT_PLANES = 0,
+  HOBF_OUT_NEXT_PLANES = 1,
+  HOBF_OUT_NEXT_RECORDS = 2,
+  HOBF_OUT_F32 = 3
+} hobf_out_mode;
 typedef struct {
   int32_t mode;     /* hobf_out_mode */
   int32_t next_wf;  /* next layer's fraction width (same exponent width we) */
@@ -208,8 +223,7 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
                            int32_t relu, hobf_epilogue ep, uint32_t* d_out, hobf_stream stream);
 
 /* hobf_conv2d_prepared with an epilogue (above) and an explicit kernel
- * schedule: variant 0 = automatic (what hobf_conv2d_prepared uses; the
- * environment variable HOBF_CONV_VARIANT overrides it there), 3 = one thread
+ * schedule: variant 0 = automatic (what hobf_conv2d_prepared uses), 3 = one thread
  * per (pixel, 32-Cout group), kernel row of 3 taps unrolled, <= 56 registers;
  * 4 = table entry of the next tap prefetched (large tables); 5 = one-warp CTAs
  * with a 3-deep prefetch ring (fewer warps than SMSPs); 6 = three kernel rows
@@ -228,6 +242,27 @@ hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t 
                                     int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout,
                                     int32_t stride, int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_out,
                                     int32_t variant, hobf_stream stream);
+
+/* ---- Which kernel a conv call runs (evidence for the measurements) ---------
+ * Runs the argument checks and the schedule choice of hobf_conv2d_ex (op 0),
+ * hobf_conv2d_prepared_ex (op 1; `variant` as there) or hobf_conv2d_dw (op 2;
+ * cin = cout = c) for these shapes, launches nothing, and fills *info with the
+ * kernel that call would launch: its symbol (mangled, cudaFuncGetName), the
+ * schedule (variant; 0 for ops 0 and 2), CTA size, CTA count, dynamic and
+ * static shared memory, registers and local (spill) bytes per thread
+ * (cudaFuncGetAttributes) and resident CTAs per SM
+ * (cudaOccupancyMaxActiveBlocksPerMultiprocessor).  Same statuses as the conv
+ * call (pointers are not needed); n = 0 -> HOBF_OK with an empty name; needs
+ * a CUDA device for the attribute queries (else HOBF_ECUDA). */
+typedef struct {
+  char name[256];
+  int32_t variant, threads, dyn_smem, static_smem, regs, local_bytes, ctas_per_sm;
+  int64_t blocks;
+} hobf_kernel_info;
+
+hobf_status hobf_conv_kernel_info(int32_t op, hobf_fmt f, int32_t n, int32_t h, int32_t w, int32_t cin, int32_t kh,
+                                  int32_t kw, int32_t cout, int32_t stride, int32_t pad, hobf_epilogue ep,
+                                  int32_t variant, hobf_kernel_info* info);
 
 /* LOP3 issue-rate microbenchmark (roofline denominator): launches `blocks` x
  * `threads` threads, each issuing `iters` x 128 dependent-free lop3 ops;

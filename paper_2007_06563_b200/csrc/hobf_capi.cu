@@ -6,7 +6,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
-#include <stdlib.h>
 
 #include <algorithm>
 
@@ -17,6 +16,8 @@
 using hobf::ConvArgs;
 using hobf::FormatEntry;
 using hobf::xrec_of;
+using hobf::decode_f32;
+using hobf::transpose32;
 
 #define HOBF_DECLARE(TAG)                                                                    \
   cudaError_t hobf_launch_conv_##TAG(const hobf::ConvArgs& a, cudaStream_t s);               \
@@ -112,36 +113,6 @@ __device__ __forceinline__ uint32_t encode_f32_fast(float f, int we, int wf, int
                         : (E < 0 || ex == 0) ? sfield : (1u << top) | sfield | ((uint32_t)E << wf) | frac;
   const uint32_t nonfinite = (u & 0x7FFFFFu) ? (3u << top) : inf;
   return ex == 0xFF ? nonfinite : finite;
-}
-
-// F(we, wf) word -> float32 (exact for we <= 7, wf <= 23).  Branch-free: the
-// four exception classes are selected, not branched on (no divergence).
-__device__ __forceinline__ float decode_f32(uint32_t v, int we, int wf) {
-  const uint32_t exc = (v >> (wf + we + 1)) & 3u;
-  const uint32_t sbit = ((v >> (wf + we)) & 1u) << 31;
-  const int E = (int)((v >> wf) & ((1u << we) - 1u)) - ((1 << (we - 1)) - 1);
-  const uint32_t frac = v & ((1u << wf) - 1u);
-  const uint32_t normal = sbit | ((uint32_t)(E + 127) << 23) | (frac << (23 - wf));
-  const uint32_t special = exc == 3u ? 0x7FC00000u : (sbit | (exc == 2u ? 0x7F800000u : 0u));
-  return __uint_as_float(exc == 1u ? normal : special);
-}
-
-// 32 x 32 bit-matrix transpose in registers (bit j of A[i] <-> bit i of A[j]):
-// five rounds of block swaps, the s x s off-diagonal blocks of every 2s x 2s
-// block exchanged with one shift and two xors per row pair.
-__device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u
-                                                                                                   : 0x55555555u;
-#pragma unroll
-    for (int i = 0; i < 32; i++) {
-      if (i & s) continue;
-      const uint32_t t = ((A[i] >> s) ^ A[i + s]) & m;
-      A[i + s] ^= t;
-      A[i] ^= t << s;
-    }
-  }
 }
 
 // ----------------------------------------------------------------------------- pack / unpack
@@ -762,6 +733,7 @@ static bool set_epilogue(ConvArgs& a, hobf_fmt f, hobf_epilogue ep, bool records
   a.next_wf = ep.next_wf;
   a.next_pad = ep.next_pad;
   if (ep.mode == HOBF_OUT_PLANES) return true;
+  if (ep.mode == HOBF_OUT_F32) return f.we <= 7;  // float32 holds every F(we <= 7, wfo <= 23) value
   if (ep.next_wf < 1 || ep.next_pad < 0) return false;
   if (ep.mode == HOBF_OUT_NEXT_PLANES) return 3 + f.we + ep.next_wf <= 32;
   if (ep.mode == HOBF_OUT_NEXT_RECORDS) return records_ok && ep.next_wf <= kTabMaxWf && 3 + f.we + ep.next_wf <= 20;
@@ -772,80 +744,127 @@ static bool set_epilogue(ConvArgs& a, hobf_fmt f, hobf_epilogue ep, bool records
 // blocks of >= 32 threads
 static const int64_t kMaxConvItems = 2147483647LL * 32;
 
-// development overrides (HOBF_CONV_VARIANT, HOBF_SMEM_CFG)
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
+enum { OP_CONV = 0, OP_PREPARED = 1, OP_DW = 2 };
+
+static const FormatEntry* tab_format(hobf_fmt f);
+
+// Shared argument checks of the conv entry points, in the order the header
+// documents: format, sizes, shapes, format support, then (n > 0 and `launch`)
+// pointers and alignment, the grid limits and the epilogue.  Fills `a` and `e`.
+// *empty is set when n == 0 (nothing to launch).
+static hobf_status conv_setup(int op, hobf_fmt f, const uint32_t* x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                              const uint32_t* wt, int32_t kh, int32_t kw, int32_t cout, int32_t stride, int32_t pad,
+                              int32_t relu, hobf_epilogue ep, void* out, int32_t variant, bool launch, ConvArgs& a,
+                              const FormatEntry*& e, bool* empty) {
+  *empty = false;
+  if (op == OP_PREPARED ? (variant != 0 && (variant < 3 || variant > 8)) : variant != 0) return HOBF_EINVAL;
+  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
+    return HOBF_EINVAL;
+  if (op == OP_DW) cout = cin;
+  if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)
+    return HOBF_EINVAL;
+  if (h == 0 || w == 0 || cin == 0 || kh == 0 || kw == 0 || cout == 0) return HOBF_ESHAPE;
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
+  if (op == OP_PREPARED && (cout + 31) / 32 > 65535) return HOBF_ESHAPE;  // output-channel groups index grid.y
+  e = op == OP_PREPARED ? tab_format(f) : find_format(f.we, f.wf, f.round, f.extended);
+  if (!e) return HOBF_EUNSUPPORTED;
+  if (n == 0) {
+    *empty = true;
+    return HOBF_OK;
+  }
+  if (launch) {
+    if (!x || !wt || !out) return HOBF_EINVAL;
+    if (!aligned16(x) || !aligned16(wt) || !aligned16(out)) return HOBF_EINVAL;
+  }
+  a = ConvArgs();
+  a.x = x; a.wt = wt; a.y = reinterpret_cast<uint32_t*>(out);
+  a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
+  a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
+  a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
+  if (a.items > kMaxConvItems) return HOBF_ESHAPE;  // one grid.x block per <= 32 items
+  a.variant = variant;
+  if (!set_epilogue(a, f, ep, op != OP_CONV)) return HOBF_EINVAL;
+  a.row_mul = 1u << 12;
+  for (int j = 0; j < 32; j++) a.lift[j] = 1u << (31 - j);
+  a.one = 1;
+  a.two = 2u;
+  a.info = nullptr;
+  return HOBF_OK;
+}
+
+static hobf_status conv_launch(int op, hobf_fmt f, const uint32_t* x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                               const uint32_t* wt, int32_t kh, int32_t kw, int32_t cout, int32_t stride, int32_t pad,
+                               int32_t relu, hobf_epilogue ep, void* out, int32_t variant, hobf_stream stream) {
+  g_last_launches = 0;
+  ConvArgs a;
+  const FormatEntry* e = nullptr;
+  bool empty = false;
+  const hobf_status st = conv_setup(op, f, x, n, h, w, cin, wt, kh, kw, cout, stride, pad, relu, ep, out, variant,
+                                    true, a, e, &empty);
+  if (st != HOBF_OK || empty) return st;
+  const hobf::conv_launcher L = op == OP_CONV ? e->conv : op == OP_PREPARED ? e->conv_tab : e->conv_dw;
+  if (L(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
+  g_last_launches = 1;
+  return HOBF_OK;
 }
 
 hobf_status hobf_conv2d(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
                         const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
                         int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
   const hobf_epilogue ep = {HOBF_OUT_PLANES, 0, 0};
-  return hobf_conv2d_ex(f, d_x_planes, n, h, w, cin, d_w_planes, kh, kw, cout, stride, pad, relu, ep, d_y_planes,
-                        stream);
+  return conv_launch(OP_CONV, f, d_x_planes, n, h, w, cin, d_w_planes, kh, kw, cout, stride, pad, relu, ep,
+                     d_y_planes, 0, stream);
 }
 
 hobf_status hobf_conv2d_ex(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t cin,
                            const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t cout, int32_t stride,
-                           int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_y_planes, hobf_stream stream) {
-  g_last_launches = 0;
-  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
-    return HOBF_EINVAL;
-  if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)
-    return HOBF_EINVAL;
-  if (h == 0 || w == 0 || cin == 0 || kh == 0 || kw == 0 || cout == 0) return HOBF_ESHAPE;
-  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
-  if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
-  const FormatEntry* e = find_format(f.we, f.wf, f.round, f.extended);
-  if (!e) return HOBF_EUNSUPPORTED;
-  if (n == 0) return HOBF_OK;
-  if (!d_x_planes || !d_w_planes || !d_y_planes) return HOBF_EINVAL;
-  if (!aligned16(d_x_planes) || !aligned16(d_w_planes) || !aligned16(d_y_planes)) return HOBF_EINVAL;
-  ConvArgs a;
-  a.x = d_x_planes; a.wt = d_w_planes; a.y = d_y_planes;
-  a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
-  a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
-  a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
-  if (a.items > kMaxConvItems) return HOBF_ESHAPE;  // one grid.x block per <= 32 items
-  a.variant = 0;
-  a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
-  if (!set_epilogue(a, f, ep, false)) return HOBF_EINVAL;
-  a.one = 1;
-  a.two = 2u;
-  if (e->conv(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
-  g_last_launches = 1;
-  return HOBF_OK;
+                           int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_out, hobf_stream stream) {
+  return conv_launch(OP_CONV, f, d_x_planes, n, h, w, cin, d_w_planes, kh, kw, cout, stride, pad, relu, ep, d_out,
+                     0, stream);
 }
 
 hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, int32_t h, int32_t w, int32_t c,
                            const uint32_t* d_w_planes, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
                            int32_t relu, hobf_epilogue ep, uint32_t* d_out, hobf_stream stream) {
-  g_last_launches = 0;
-  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
-    return HOBF_EINVAL;
-  if (n < 0 || h < 0 || w < 0 || c < 0 || kh < 0 || kw < 0 || stride <= 0 || pad < 0) return HOBF_EINVAL;
-  if (h == 0 || w == 0 || c == 0 || kh == 0 || kw == 0) return HOBF_ESHAPE;
-  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
-  if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
-  const FormatEntry* e = find_format(f.we, f.wf, f.round, f.extended);
-  if (!e) return HOBF_EUNSUPPORTED;
-  if (n == 0) return HOBF_OK;
-  if (!d_x_planes || !d_w_planes || !d_out) return HOBF_EINVAL;
-  if (!aligned16(d_x_planes) || !aligned16(d_w_planes) || !aligned16(d_out)) return HOBF_EINVAL;
+  return conv_launch(OP_DW, f, d_x_planes, n, h, w, c, d_w_planes, kh, kw, c, stride, pad, relu, ep, d_out, 0,
+                     stream);
+}
+
+hobf_status hobf_conv_kernel_info(int32_t op, hobf_fmt f, int32_t n, int32_t h, int32_t w, int32_t cin, int32_t kh,
+                                  int32_t kw, int32_t cout, int32_t stride, int32_t pad, hobf_epilogue ep,
+                                  int32_t variant, hobf_kernel_info* info) {
+  if (!info || op < OP_CONV || op > OP_DW) return HOBF_EINVAL;
+  *info = hobf_kernel_info();
   ConvArgs a;
-  a.x = d_x_planes; a.wt = d_w_planes; a.y = d_out;
-  a.n = n; a.h = h; a.w = w; a.cin = c; a.kh = kh; a.kw = kw; a.cout = c;
-  a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
-  a.items = (int64_t)n * ho * wo * ((c + 31) / 32);
-  if (a.items > kMaxConvItems) return HOBF_ESHAPE;  // one grid.x block per <= 32 items
-  a.variant = 0;
-  a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
-  if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;
-  a.one = 1;
-  a.two = 2u;
-  if (e->conv_dw(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
-  g_last_launches = 1;
+  const FormatEntry* e = nullptr;
+  bool empty = false;
+  hobf_status st = conv_setup(op, f, nullptr, n, h, w, cin, nullptr, kh, kw, cout, stride, pad, 0, ep, nullptr,
+                              variant, false, a, e, &empty);
+  if (st != HOBF_OK || empty) return st;
+  hobf::LaunchInfo li = {};
+  a.info = &li;
+  const hobf::conv_launcher L = op == OP_CONV ? e->conv : op == OP_PREPARED ? e->conv_tab : e->conv_dw;
+  if (L(a, nullptr) != cudaSuccess || !li.func) return HOBF_ECUDA;
+  info->variant = li.variant;
+  info->threads = li.threads;
+  info->dyn_smem = (int32_t)li.smem;
+  info->blocks = li.blocks;
+  const char* name = nullptr;
+  if (cudaFuncGetName(&name, li.func) == cudaSuccess && name) {
+    snprintf(info->name, sizeof(info->name), "%s", name);
+  }
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, li.func) != cudaSuccess) return HOBF_ECUDA;
+  info->regs = fa.numRegs;
+  info->local_bytes = (int32_t)fa.localSizeBytes;
+  info->static_smem = (int32_t)fa.sharedSizeBytes;
+  if (li.smem > 48 * 1024)
+    cudaFuncSetAttribute(li.func, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, li.func, li.threads, li.smem) != cudaSuccess)
+    return HOBF_ECUDA;
+  info->ctas_per_sm = nb;
   return HOBF_OK;
 }
 
@@ -872,16 +891,6 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
   if (relu) *relu = e->g_relu;
   if (mac_tab) *mac_tab = e->g_tab;
   return HOBF_OK;
-}
-
-// Kernel variant of hobf_conv2d_prepared (see launch_conv_tab); HOBF_CONV_VARIANT overrides.
-static int conv_tab_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HOBF_CONV_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
 }
 
 static const FormatEntry* tab_format(hobf_fmt f) {
@@ -952,9 +961,11 @@ hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, i
   const int cc = (int)std::min<int64_t>(std::min<int64_t>(cin, 256),
                                         std::max<int64_t>(4, (32 * 1024 / 4) / stride) / 4 * 4);
   const int64_t kMaxGrid = 2147483647LL;
-  if ((cin & 3) == 0 && aligned16(d_x)) {
+  const size_t smem = (size_t)cc * stride * 4;
+  // row kernels: float4 channel quads, the row's records transposed in at most the
+  // default 48 KB of shared memory (w up to 3071); wider rows take the tile kernel
+  if ((cin & 3) == 0 && aligned16(d_x) && smem <= 48 * 1024) {
     const int chunks = (cin + cc - 1) / cc;
-    const size_t smem = (size_t)cc * stride * 4;
     if (n <= 65535 && chunks <= 65535) {
       quantize_acts_row_kernel<<<dim3((unsigned)Hp, (unsigned)n, (unsigned)chunks), 256, smem,
                                  (cudaStream_t)stream>>>(d_x, n, h, w, cin, pad, f.we, f.wf, f.round, cc, stride,
@@ -979,45 +990,15 @@ hobf_status hobf_conv2d_prepared(hobf_fmt f, const uint32_t* d_xrec, int32_t n, 
                                  int32_t pad, int32_t relu, uint32_t* d_y_planes, hobf_stream stream) {
   const hobf_epilogue ep = {HOBF_OUT_PLANES, 0, 0};
   return hobf_conv2d_prepared_ex(f, d_xrec, n, h, w, cin, d_wtab, kh, kw, cout, stride, pad, relu, ep, d_y_planes,
-                                 conv_tab_variant(), stream);
+                                 0, stream);
 }
 
 hobf_status hobf_conv2d_prepared_ex(hobf_fmt f, const uint32_t* d_xrec, int32_t n, int32_t h, int32_t w,
                                     int32_t cin, const uint32_t* d_wtab, int32_t kh, int32_t kw, int32_t cout,
-                                    int32_t stride, int32_t pad, int32_t relu, hobf_epilogue ep,
-                                    uint32_t* d_y_planes, int32_t variant, hobf_stream stream) {
-  const uint32_t* d_x_planes = d_xrec;
-  g_last_launches = 0;
-  if (variant != 0 && (variant < 3 || variant > 8)) return HOBF_EINVAL;
-  if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
-    return HOBF_EINVAL;
-  if (n < 0 || h < 0 || w < 0 || cin < 0 || kh < 0 || kw < 0 || cout < 0 || stride <= 0 || pad < 0)
-    return HOBF_EINVAL;
-  if (h == 0 || w == 0 || cin == 0 || kh == 0 || kw == 0 || cout == 0) return HOBF_ESHAPE;
-  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
-  if (h + 2 * pad < kh || w + 2 * pad < kw || ho <= 0 || wo <= 0) return HOBF_ESHAPE;
-  if ((cout + 31) / 32 > 65535) return HOBF_ESHAPE;  // output-channel groups index grid.y
-  const FormatEntry* e = tab_format(f);
-  if (!e) return HOBF_EUNSUPPORTED;
-  if (n == 0) return HOBF_OK;
-  if (!d_x_planes || !d_wtab || !d_y_planes) return HOBF_EINVAL;
-  if (!aligned16(d_x_planes) || !aligned16(d_wtab) || !aligned16(d_y_planes)) return HOBF_EINVAL;
-  ConvArgs a;
-  a.x = d_x_planes; a.wt = d_wtab; a.y = d_y_planes;
-  a.n = n; a.h = h; a.w = w; a.cin = cin; a.kh = kh; a.kw = kw; a.cout = cout;
-  a.stride = stride; a.pad = pad; a.relu = relu ? 1 : 0; a.ho = ho; a.wo = wo;
-  a.items = (int64_t)n * ho * wo * ((cout + 31) / 32);
-  if (a.items > kMaxConvItems) return HOBF_ESHAPE;  // one grid.x block per <= 32 items
-  a.variant = variant;
-  a.smem_cfg = env_int("HOBF_SMEM_CFG", 0);
-  if (!set_epilogue(a, f, ep, true)) return HOBF_EINVAL;
-  a.row_mul = 1u << 12;
-  for (int j = 0; j < 32; j++) a.lift[j] = 1u << (31 - j);
-  a.one = 1;
-  a.two = 2u;
-  if (e->conv_tab(a, (cudaStream_t)stream) != cudaSuccess) return HOBF_ECUDA;
-  g_last_launches = 1;
-  return HOBF_OK;
+                                    int32_t stride, int32_t pad, int32_t relu, hobf_epilogue ep, uint32_t* d_out,
+                                    int32_t variant, hobf_stream stream) {
+  return conv_launch(OP_PREPARED, f, d_xrec, n, h, w, cin, d_wtab, kh, kw, cout, stride, pad, relu, ep, d_out,
+                     variant, stream);
 }
 
 hobf_status hobf_lop3_peak(int32_t blocks, int32_t threads, int32_t iters, uint32_t* d_sink, hobf_stream stream,

@@ -110,9 +110,43 @@ __device__ __forceinline__ void store_requant(const uint32_t* acc, const ConvArg
   }
 }
 
+// out_mode 3 (HOBF_OUT_F32, the last layer): the 32 lanes' words, by a
+// register bit transpose of the NOUT planes, decoded to their exact float32
+// values and stored NHWC -- the 32 channels of the group are 128 contiguous
+// bytes (eight 16-byte stores when cout % 4 == 0).  No plane round trip.
+template <class F>
+__device__ __forceinline__ void store_f32(const uint32_t* acc, const ConvArgs& a, int64_t pix, int g) {
+  uint32_t A[32];
+#pragma unroll
+  for (int j = 0; j < 32; j++) A[j] = j < F::NOUT ? acc[j % F::NOUT] : 0u;
+  transpose32(A);  // A[l] = word of lane l
+  float* base = reinterpret_cast<float*>(a.y) + pix * a.cout + 32 * g;
+  const int nl = min(32, a.cout - 32 * g);
+  if ((a.cout & 3) == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if (4 * q >= nl) break;
+      float4 v;
+      v.x = decode_f32(A[4 * q + 0], F::WE, F::WFO);
+      v.y = decode_f32(A[4 * q + 1], F::WE, F::WFO);
+      v.z = decode_f32(A[4 * q + 2], F::WE, F::WFO);
+      v.w = decode_f32(A[4 * q + 3], F::WE, F::WFO);
+      reinterpret_cast<float4*>(base)[q] = v;
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < 32; l++)
+      if (l < nl) base[l] = decode_f32(A[l], F::WE, F::WFO);
+  }
+}
+
 template <class F>
 __device__ __forceinline__ void store_out(const uint32_t* acc, const ConvArgs& a, int64_t pix, int g, int ni, int oy,
                                           int ox) {
+  if (a.out_mode == 3) {
+    if constexpr (F::WE <= 7) store_f32<F>(acc, a, pix, g);
+    return;
+  }
   if (a.out_mode != 0) {
     store_requant<F>(acc, a, pix, g, ni, oy, ox);
     return;
@@ -705,6 +739,23 @@ inline void allow_big_smem(const void* kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
+// Launch `kern`, or -- when a.info is set (hobf_conv_kernel_info) -- only record
+// which kernel and launch shape the schedule chose.
+template <class K>
+cudaError_t run(const ConvArgs& a, K kern, dim3 grid, int threads, size_t smem, cudaStream_t s, int variant) {
+  if (a.info) {
+    a.info->func = (const void*)kern;
+    a.info->variant = variant;
+    a.info->threads = threads;
+    a.info->smem = smem;
+    a.info->blocks = (int64_t)grid.x * grid.y * grid.z;
+    return cudaSuccess;
+  }
+  if (smem > 48 * 1024) allow_big_smem((const void*)kern);
+  kern<<<grid, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <class F>
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   if (a.items == 0) return cudaSuccess;
@@ -715,10 +766,9 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
   // 0.70 of the roof vs 6), wF = 7, 8 6 (<= 80), wF >= 9 4 (<= 128: e5m10 0.60 -> 0.66)
   constexpr int GM = F::WF >= 9 ? 4 : (F::WF >= 7 ? 6 : 5);
   if (a.kh == 3 && a.kw == 3)
-    conv_direct_kernel<F, GM, true><<<(unsigned)blocks, threads, 0, s>>>(a);
+    return run(a, conv_direct_kernel<F, GM, true>, dim3((unsigned)blocks), threads, 0, s, 0);
   else
-    conv_direct_kernel<F><<<(unsigned)blocks, threads, 0, s>>>(a);
-  return cudaGetLastError();
+    return run(a, conv_direct_kernel<F>, dim3((unsigned)blocks), threads, 0, s, 0);
 }
 
 template <class F>
@@ -755,54 +805,41 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   if (variant == 8) {
     if constexpr (F::WF >= 5 && F::WF <= 9) {
       const int64_t ub = ut == 3 ? row_bytes : tap_bytes;
-      auto go = [&](auto kern) {
-        allow_big_smem((const void*)kern);
-        kern<<<grid(256), 256, (size_t)(2 * ub), s>>>(a);
-      };
+      auto go = [&](auto kern) { return run(a, kern, grid(256), 256, (size_t)(2 * ub), s, 8); };
       // 256-thread CTAs, 3 per SM (80 registers; measured on C5: 4 per SM at 64
       // registers, 512-thread CTAs and per-channel staging at 2 CTAs / SM are slower)
-      if (ut == 3) go(conv_tab_smem_kernel<F, 256, 3, 1, true, 3>);
-      else if (6 * ub <= 216 * 1024) go(conv_tab_smem_kernel<F, 256, 3, 1, true, 1>);
-      else go(conv_tab_smem_kernel<F, 256, 2, 1, true, 1>);
+      if (ut == 3) return go(conv_tab_smem_kernel<F, 256, 3, 1, true, 3>);
+      if (6 * ub <= 216 * 1024) return go(conv_tab_smem_kernel<F, 256, 3, 1, true, 1>);
+      return go(conv_tab_smem_kernel<F, 256, 2, 1, true, 1>);
     }
     return cudaGetLastError();
   }
   if (variant == 7) {
-    const int sm = a.smem_cfg;  // development override (HOBF_SMEM_CFG): 0 auto, 2, 3, 6 or 7
     // 3x3 with >= 8 warps per SMSP of work: 128-thread CTAs x 6 per SM at <= 80
     // registers (C3 0.846 / C4 0.887 of the roof, vs 0.827 / 0.869 at 8 x 64 registers);
     // fewer warps (single partial wave): 256-thread CTAs x 3 (MOB 0.785 vs 0.767, C5
     // +1%); measured, DESIGN.md section 6
-    const int cfg = sm ? sm : (warps >= 148 * 4 * 8 && 12 * blk_bytes <= 216 * 1024) ? 6 : 7;
-    auto go = [&](auto kern, int nt, int cc) {
-      allow_big_smem((const void*)kern);
-      kern<<<grid(nt), nt, (size_t)(2 * cc * blk_bytes), s>>>(a);
-    };
+    const int cfg = (warps >= 148 * 4 * 8 && 12 * blk_bytes <= 216 * 1024) ? 6 : 7;
+    auto go = [&](auto kern, int nt, int cc) { return run(a, kern, grid(nt), nt, (size_t)(2 * cc * blk_bytes), s, 7); };
     if (k33) {
-      if (cfg == 6) go(conv_tab_smem_kernel<F, 128, 6, 1, true>, 128, 1);
-      else if (cfg == 2) go(conv_tab_smem_kernel<F, 128, 8, 1, true>, 128, 1);
-      else if (cfg == 3) go(conv_tab_smem_kernel<F, 256, 4, 1, true>, 256, 1);
-      else go(conv_tab_smem_kernel<F, 256, 3, 1, true>, 256, 1);
-    } else {
-      go(conv_tab_smem_kernel<F, 256, 4, 1, false>, 256, 1);
+      if (cfg == 6) return go(conv_tab_smem_kernel<F, 128, 6, 1, true>, 128, 1);
+      return go(conv_tab_smem_kernel<F, 256, 3, 1, true>, 256, 1);
     }
-    return cudaGetLastError();
+    return go(conv_tab_smem_kernel<F, 256, 4, 1, false>, 256, 1);
   }
   if (variant == 6 && k3) {  // KW=3, 3 kernel rows (one input channel) per unrolled body, <= 64 registers
-    conv_tab_kernel<F, 128, 8, true, 0, 3><<<grid(128), 128, 0, s>>>(a);
+    return run(a, conv_tab_kernel<F, 128, 8, true, 0, 3>, grid(128), 128, 0, s, 6);
   } else if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
-    conv_tab_kernel<F, 32, 1, false, 3><<<grid(32), 32, 0, s>>>(a);
+    return run(a, conv_tab_kernel<F, 32, 1, false, 3>, grid(32), 32, 0, s, 5);
   } else if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
     // <= 96 registers, 5 CTAs / SM (C3 e5m10 0.79 -> 0.81, C5 wF = 10 +0-3% vs 128 registers);
     // the extended class's largest circuits (> 400 lop3) get 128 (4 CTAs / SM)
     constexpr int M4 = F::G_TAB > 400 ? 4 : 5;
-    conv_tab_kernel<F, 128, M4, false, 1><<<grid(128), 128, 0, s>>>(a);
+    return run(a, conv_tab_kernel<F, 128, M4, false, 1>, grid(128), 128, 0, s, 4);
   } else if (k3) {     // kernel width 3 unrolled, <= 56 registers (9 CTAs / SM)
-    conv_tab_kernel<F, 128, 9, true, 0><<<grid(128), 128, 0, s>>>(a);
-  } else {
-    conv_tab_kernel<F, 128, 9, false, 0><<<grid(128), 128, 0, s>>>(a);
+    return run(a, conv_tab_kernel<F, 128, 9, true, 0>, grid(128), 128, 0, s, 3);
   }
-  return cudaGetLastError();
+  return run(a, conv_tab_kernel<F, 128, 9, false, 0>, grid(128), 128, 0, s, 3);
 }
 
 template <class F>
@@ -812,9 +849,8 @@ cudaError_t launch_conv_dw(const ConvArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)((a.items + threads - 1) / threads);
   // 3x3: nine taps in one body at <= 128 registers (MOBDW conv 0.63 -> 0.65 of the roof;
   // 5 or 6 CTAs / SM at 96 / 80 registers: 0.62 / 0.63)
-  if (a.kh == 3 && a.kw == 3) conv_dw_kernel<F, 4, true><<<blocks, threads, 0, s>>>(a);
-  else conv_dw_kernel<F><<<blocks, threads, 0, s>>>(a);
-  return cudaGetLastError();
+  if (a.kh == 3 && a.kw == 3) return run(a, conv_dw_kernel<F, 4, true>, dim3(blocks), threads, 0, s, 0);
+  return run(a, conv_dw_kernel<F>, dim3(blocks), threads, 0, s, 0);
 }
 
 template <class F>

@@ -61,4 +61,34 @@ __host__ __device__ constexpr int tab_stride(int npt, int wf) {
   return (wf > 7 || ((npt / 4) & 1)) ? npt : npt + 4;
 }
 
+// F(we, wf) word -> float32 (exact for we <= 7, wf <= 23).  Branch-free: the
+// four exception classes are selected, not branched on (no divergence).
+__device__ __forceinline__ float decode_f32(uint32_t v, int we, int wf) {
+  const uint32_t exc = (v >> (wf + we + 1)) & 3u;
+  const uint32_t sbit = ((v >> (wf + we)) & 1u) << 31;
+  const int E = (int)((v >> wf) & ((1u << we) - 1u)) - ((1 << (we - 1)) - 1);
+  const uint32_t frac = v & ((1u << wf) - 1u);
+  const uint32_t normal = sbit | ((uint32_t)(E + 127) << 23) | (frac << (23 - wf));
+  const uint32_t special = exc == 3u ? 0x7FC00000u : (sbit | (exc == 2u ? 0x7F800000u : 0u));
+  return __uint_as_float(exc == 1u ? normal : special);
+}
+
+// 32 x 32 bit-matrix transpose in registers (bit j of A[i] <-> bit i of A[j]):
+// five rounds of block swaps, the s x s off-diagonal blocks of every 2s x 2s
+// block exchanged with one shift and two xors per row pair.
+__device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u
+                                                                                                   : 0x55555555u;
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      if (i & s) continue;
+      const uint32_t t = ((A[i] >> s) ^ A[i + s]) & m;
+      A[i + s] ^= t;
+      A[i] ^= t << s;
+    }
+  }
+}
+
 }  // namespace hobf

@@ -42,7 +42,7 @@ class hobf_epilogue(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("next_wf", ctypes.c_int32), ("next_pad", ctypes.c_int32)]
 
 
-OUT_PLANES, OUT_NEXT_PLANES, OUT_NEXT_RECORDS = 0, 1, 2
+OUT_PLANES, OUT_NEXT_PLANES, OUT_NEXT_RECORDS, OUT_F32 = 0, 1, 2, 3
 
 
 @dataclass(frozen=True)
@@ -56,6 +56,19 @@ class Next:
 
     def c(self) -> hobf_epilogue:
         return hobf_epilogue(OUT_NEXT_RECORDS if self.records else OUT_NEXT_PLANES, self.wf, self.pad)
+
+
+@dataclass(frozen=True)
+class Float32Out:
+    """Last-layer epilogue (HOBF_OUT_F32): the conv writes its outputs as exact
+    float32 NHWC [n*ho*wo, cout] instead of planes (no unpack pass)."""
+    records = False
+
+    def c(self) -> hobf_epilogue:
+        return hobf_epilogue(OUT_F32, 0, 0)
+
+
+F32 = Float32Out()
 
 
 @dataclass(frozen=True)
@@ -126,6 +139,15 @@ _lib.hobf_prepare_activations.restype = _i32
 _lib.hobf_prepare_activations.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _i32, _p, _p]
 _lib.hobf_quantize_activations.restype = _i32
 _lib.hobf_quantize_activations.argtypes = [hobf_fmt, _p, _i32, _i32, _i32, _i32, _i32, _p, _p]
+class hobf_kernel_info(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 256), ("variant", _i32), ("threads", _i32), ("dyn_smem", _i32),
+                ("static_smem", _i32), ("regs", _i32), ("local_bytes", _i32), ("ctas_per_sm", _i32),
+                ("blocks", _i64)]
+
+
+_lib.hobf_conv_kernel_info.restype = _i32
+_lib.hobf_conv_kernel_info.argtypes = [_i32, hobf_fmt, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                       hobf_epilogue, _i32, ctypes.POINTER(hobf_kernel_info)]
 _lib.hobf_lop3_peak.restype = _i32
 _lib.hobf_lop3_peak.argtypes = [_i32, _i32, _i32, _p, _p, ctypes.POINTER(_i64)]
 _lib.hobf_last_launch_count.restype = _i32
@@ -137,7 +159,7 @@ SYMBOLS = ["hobf_nbits", "hobf_out_wf", "hobf_nplanes", "hobf_planes_words", "ho
            "hobf_unpack", "hobf_unpack_f32", "hobf_conv2d", "hobf_mac_planes", "hobf_gate_count",
            "hobf_lop3_peak", "hobf_last_launch_count", "hobf_status_str", "hobf_version",
            "hobf_wtab_words", "hobf_prepare_weights", "hobf_conv2d_prepared", "hobf_conv2d_prepared_ex", "hobf_conv2d_ex", "hobf_conv2d_dw", "hobf_xrec_words",
-           "hobf_prepare_activations", "hobf_quantize_activations"]
+           "hobf_prepare_activations", "hobf_quantize_activations", "hobf_conv_kernel_info"]
 
 
 def _check(fn, st):
@@ -229,6 +251,10 @@ def _next_out(f: Fmt, nxt, n, ho, wo, cout, device, out):
     """Output buffer of a conv with epilogue `nxt` (None = plain output planes)."""
     if nxt is None:
         return _new_planes(max(n * ho * wo, 0), cout, f.nout, device, out)
+    if isinstance(nxt, Float32Out):
+        if out is None:
+            out = torch.empty((max(n * ho * wo, 0), cout), dtype=torch.float32, device=device)
+        return out
     if not nxt.records:
         return _new_planes(max(n * ho * wo, 0), cout, nbits(f.we, nxt.wf), device, out)
     if out is None:  # the +0 border of the next layer's records: (2^wf) << 20
@@ -242,7 +268,8 @@ def conv2d(f: Fmt, x_planes: torch.Tensor, n: int, h: int, w: int, cin: int, w_p
            stream=None, nxt: "Next | None" = None) -> torch.Tensor:
     """HOBFLOPS conv on planes; returns output planes [n*ho*wo, ceil(cout/32), NP(NOUT)],
     or with nxt = Next(wf, records=False) the next layer's input planes of F(we, wf)
-    (hobf_conv2d_ex, fused re-rounding epilogue)."""
+    (hobf_conv2d_ex, fused re-rounding epilogue), or with nxt = F32 the exact float32
+    outputs [n*ho*wo, cout] (HOBF_OUT_F32)."""
     ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
     out = _next_out(f, nxt, n, ho, wo, cout, x_planes.device, out)
     if nxt is None:
@@ -330,7 +357,8 @@ def conv2d_prepared(f: Fmt, xrec: torch.Tensor, n: int, h: int, w: int, cin: int
     """Conv on prepared activations (same pad) and prepared weights -> output planes.
     variant: None = automatic kernel schedule, else that schedule (identical results);
     nxt: Next(wf, records=True, pad) writes the next layer's activation records
-    (or planes) of F(we, wf) instead (hobf_conv2d_prepared_ex, fused re-rounding)."""
+    (or planes) of F(we, wf) instead (hobf_conv2d_prepared_ex, fused re-rounding);
+    nxt = F32 writes the exact float32 outputs [n*ho*wo, cout] (HOBF_OUT_F32)."""
     ho, wo = conv_out_hw(h, w, kh, kw, stride, pad)
     out = _next_out(f, nxt, n, ho, wo, cout, xrec.device, out)
     if variant is None and nxt is None:
@@ -343,6 +371,22 @@ def conv2d_prepared(f: Fmt, xrec: torch.Tensor, n: int, h: int, w: int, cin: int
                _lib.hobf_conv2d_prepared_ex(f.c(), _ptr(xrec), n, h, w, cin, _ptr(wtab), kh, kw, cout, stride,
                                             pad, int(relu), ep, _ptr(out), int(variant or 0), _stream(stream)))
     return out
+
+
+OP_CONV, OP_PREPARED, OP_DW = 0, 1, 2
+
+
+def conv_kernel_info(op: int, f: Fmt, n: int, h: int, w: int, cin: int, kh: int, kw: int, cout: int,
+                     stride: int = 1, pad: int = 1, nxt=None, variant: int = 0) -> dict:
+    """The kernel (symbol, schedule, CTA shape, registers, spills, CTAs per SM) that the
+    conv call with these arguments launches (hobf_conv_kernel_info; nothing is launched)."""
+    info = hobf_kernel_info()
+    ep = nxt.c() if nxt is not None else hobf_epilogue(OUT_PLANES, 0, 0)
+    _check("hobf_conv_kernel_info", _lib.hobf_conv_kernel_info(op, f.c(), n, h, w, cin, kh, kw, cout, stride, pad, ep,
+                                                               variant, ctypes.byref(info)))
+    return {"name": info.name.decode(), "variant": info.variant, "threads": info.threads,
+            "dyn_smem": info.dyn_smem, "static_smem": info.static_smem, "regs": info.regs,
+            "local_bytes": info.local_bytes, "ctas_per_sm": info.ctas_per_sm, "blocks": info.blocks}
 
 
 def lop3_peak(blocks: int, threads: int, iters: int, sink: torch.Tensor, stream=None) -> int:
@@ -386,13 +430,14 @@ class Conv2d:
         if not x_f32.is_cuda:
             x_f32 = x_f32.to(self.w_planes.device)
         x_f32 = x_f32.to(torch.float32)
+        # the conv's float32 epilogue writes the NHWC output directly (no plane round trip)
         if self.wtab is not None:
             xrec = quantize_activations(self.f, x_f32.contiguous(), self.pad)
-            yp = conv2d_prepared(self.f, xrec, n, h, w, cin, self.wtab, self.kh, self.kw, self.cout, self.stride,
-                                 self.pad, int(self.relu))
+            y = conv2d_prepared(self.f, xrec, n, h, w, cin, self.wtab, self.kh, self.kw, self.cout, self.stride,
+                                self.pad, int(self.relu), nxt=F32)
         else:
             xp = quantize_pack(self.f.we, self.f.wf, x_f32.reshape(n * h * w, cin).contiguous(), self.f.round)
-            yp = self.forward_planes(xp, n, h, w)
+            y = conv2d(self.f, xp, n, h, w, cin, self.w_planes, self.kh, self.kw, self.cout, self.stride, self.pad,
+                       int(self.relu), nxt=F32)
         ho, wo = conv_out_hw(h, w, self.kh, self.kw, self.stride, self.pad)
-        y = unpack_f32(self.f.we, self.f.wfo, yp, n * ho * wo, self.cout)
         return y.reshape(n, ho, wo, self.cout)

@@ -84,6 +84,21 @@ def test_argument_errors_are_synchronous_and_need_no_gpu():
     assert lib.hobf_conv2d_prepared_ex(f, P, big, 4096, 4096, 4, P, 3, 3, 32, 1, 1, 0, E(0, 0, 0), P, 0, None) == 2
     assert lib.hobf_conv2d_ex(f, P, big, 4096, 4096, 4, P, 3, 3, 32, 1, 1, 0, E(0, 0, 0), P, None) == 2
     assert lib.hobf_conv2d_dw(f, P, big, 4096, 4096, 32, P, 3, 3, 1, 1, 0, E(0, 0, 0), P, None) == 2
+    # the float32 output epilogue needs we <= 7 (exact float32 values); a misaligned output is refused
+    f83 = hobf.Fmt(8, 3).c()
+    assert lib.hobf_conv2d_ex(f83, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(hobf.OUT_F32, 0, 0), P, None) in (1, 3)
+    assert lib.hobf_conv2d_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(hobf.OUT_F32, 0, 0), P + 4, None) == 1
+    # the kernel-info query checks its arguments like the conv calls
+    info = hobf.hobf_kernel_info()
+    assert lib.hobf_conv_kernel_info(3, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 0, ctypes.byref(info)) == 1
+    assert lib.hobf_conv_kernel_info(1, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 0, None) == 1
+    assert lib.hobf_conv_kernel_info(1, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 11, ctypes.byref(info)) == 1
+    assert lib.hobf_conv_kernel_info(0, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 4, ctypes.byref(info)) == 1
+    assert lib.hobf_conv_kernel_info(1, f, 1, 2, 2, 4, 5, 5, 8, 1, 0, E(0, 0, 0), 0, ctypes.byref(info)) == 2
+    assert lib.hobf_conv_kernel_info(1, hobf.Fmt(7, 3).c(), 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 0,
+                                     ctypes.byref(info)) == 3
+    assert lib.hobf_conv_kernel_info(1, f, 0, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 0, ctypes.byref(info)) == 0
+    assert info.name == b""
 
 
 def test_binding_fails_loudly_without_library(tmp_path):

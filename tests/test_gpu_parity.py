@@ -660,3 +660,86 @@ def test_mobilenets_layer_sampled(name):
         idx = np.random.default_rng(3).integers(0, y.size, 512)
         exp = oracle.conv2d_sample(xq, wq, idx, we, wf, wf + 1, 0, cfg.stride, cfg.pad, 0)
         assert np.array_equal(y.ravel()[idx], exp)
+
+
+# ----------------------------------------------------------------------------- float32 output epilogue (HOBF_OUT_F32)
+
+def _f32_bits(t):
+    return t.contiguous().cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("we,wf,ext", [(5, 3, 0), (4, 3, 0), (5, 10, 0), (6, 7, 0), (5, 3, 1), (6, 10, 1)])
+@pytest.mark.parametrize("cout", [64, 40, 33])
+def test_f32_epilogue_matches_oracle_decode(we, wf, ext, cout):
+    """conv -> exact float32 NHWC in the conv's epilogue (no planes): every float's
+    bits equal the oracle's words decoded (decode_f64 -> float32 is exact for
+    we <= 7), for the gate kernel, every prepared schedule and the depthwise
+    kernel; cout % 4 == 0 (16-byte stores) and ragged (scalar stores)."""
+    H = hobf()
+    n, h, w, cin = 2, 9, 11, 20
+    x, wt = inputs.small_case(900 + cout + wf, n, h, w, cin, cout, "normal", 0.4)
+    x[0, 0, :3, 0] = [np.inf, np.nan, -0.0]
+    wt[0, 0, 1, :2] = [np.inf, 0.0]
+    for rnd in (0, 1):
+        f = H.Fmt(we, wf, rnd, extended=ext)
+        for relu in (0, 1):
+            exp_w = oracle_conv(x, wt, f, relu=relu).reshape(-1, cout)
+            exp = oracle.decode_f64(exp_w, we, f.wfo).astype(np.float32).view(np.uint32)
+            xp = H.quantize_pack(we, wf, torch.from_numpy(x.reshape(-1, cin)).cuda(), rnd)
+            wp = H.quantize_pack(we, wf, torch.from_numpy(wt.reshape(-1, cout)).cuda(), rnd)
+            got = _f32_bits(H.conv2d(f, xp, n, h, w, cin, wp, 3, 3, cout, 1, 1, relu, nxt=H.F32))
+            assert np.array_equal(got, exp), ("gates", rnd, relu)
+            if H.wtab_words(f, 3, 3, cin, cout) > 0:
+                tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
+                xr = H.quantize_activations(f, torch.from_numpy(x).cuda(), 1)
+                for variant in (0, 4, 5, 6, 7, 8):
+                    got = _f32_bits(H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, relu,
+                                                      variant=variant, nxt=H.F32))
+                    assert np.array_equal(got, exp), ("tables", variant, rnd, relu)
+    # depthwise
+    xd, wd = inputs.small_case(950 + cout, n, h, w, cout, cout, "normal", 0.5, dw=True)
+    f = H.Fmt(we, wf, 0, extended=ext)
+    exp_w = oracle.conv2d_dw(oracle.encode_f32(xd, we, wf), oracle.encode_f32(wd, we, wf), we, wf, f.wfo, 0, 2, 1, 1)
+    exp = oracle.decode_f64(exp_w.reshape(-1, cout), we, f.wfo).astype(np.float32).view(np.uint32)
+    xp = H.quantize_pack(we, wf, torch.from_numpy(xd.reshape(-1, cout)).cuda(), 0)
+    wp = H.quantize_pack(we, wf, torch.from_numpy(wd.reshape(-1, cout)).cuda(), 0)
+    got = _f32_bits(H.conv2d_dw(f, xp, n, h, w, cout, wp, 3, 3, 2, 1, 1, nxt=H.F32))
+    assert np.array_equal(got, exp)
+
+
+def test_f32_epilogue_rejects_wide_exponent():
+    H = hobf()
+    z = torch.zeros(1 << 12, dtype=torch.int32, device="cuda")
+    with pytest.raises(H.HobfError) as e:
+        H.conv2d(H.Fmt(8, 3), z, 1, 4, 4, 4, z, 3, 3, 32, 1, 1, 0, out=torch.zeros(512, device="cuda"), nxt=H.F32)
+    assert e.value.status in (1, 3)
+
+
+def test_quantize_activations_wide_rows():
+    """Rows of >= 3072 columns with cin % 4 == 0: the row kernel's transposed records
+    would need > 48 KB of shared memory, so the call takes the tile kernel."""
+    H = hobf()
+    rng = np.random.default_rng(33)
+    for (n, h, w, cin) in [(1, 2, 4096, 8), (2, 3, 3071, 4), (1, 1, 5000, 12)]:
+        x = rng.standard_normal((n, h, w, cin)).astype(np.float32)
+        for pad in (0, 1):
+            f = H.Fmt(5, 3, 0)
+            rec = to_np_words(H.quantize_activations(f, torch.from_numpy(x).cuda(), pad))
+            rec = rec.reshape(n, cin, h + 2 * pad, w + 2 * pad)
+            inner = rec[:, :, pad:pad + h, pad:pad + w] & np.uint32((1 << 20) - 1)
+            assert np.array_equal(inner.transpose(0, 2, 3, 1), oracle.encode_f32(x, 5, 3, 0))
+
+
+def test_conv_kernel_info_reports_the_launch():
+    """hobf_conv_kernel_info names the kernel the bench's launch runs (symbol, schedule,
+    CTA shape, registers, no spills, resident CTAs) without launching anything."""
+    H = hobf()
+    c3 = inputs.CONFIGS["C3"]
+    k = H.conv_kernel_info(H.OP_PREPARED, H.Fmt(5, 3, 0), c3.n, 56, 56, 64, 3, 3, 64, 1, 1, nxt=H.F32)
+    assert k["variant"] == 7 and k["threads"] == 128 and "conv_tab_smem_kernel" in k["name"]
+    assert k["ctas_per_sm"] == 6 and k["regs"] <= 80 and k["local_bytes"] == 0
+    assert k["blocks"] == (c3.n * 56 * 56 + 127) // 128 * 2
+    k2 = H.conv_kernel_info(H.OP_PREPARED, H.Fmt(5, 10, 0), 1, 56, 56, 64, 3, 3, 64, 1, 1)
+    assert k2["variant"] == 5 and k2["threads"] == 32
+    kd = H.conv_kernel_info(H.OP_DW, H.Fmt(5, 3, 0), 2, 14, 14, 512, 3, 3, 512, 2, 1)
+    assert "conv_dw_kernel" in kd["name"] and kd["local_bytes"] == 0

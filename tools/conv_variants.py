@@ -1,6 +1,6 @@
 """Kernel-only timing of the conv kernels (development tool, not the bench).
 
-    HOBF_CONV_VARIANT=3 python tools/conv_variants.py --config C3 [--kernel tables|gates]
+    python tools/conv_variants.py --config C3 [--kernel tables|gates] [--variant 3]
 Prints one JSON line: conv ms (CUDA events, median of reps), MAC/s, lop3 frac.
 """
 import argparse
@@ -22,6 +22,7 @@ ap.add_argument("--format", default=None)
 ap.add_argument("--kernel", default="tables")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--round", type=int, default=0)
+ap.add_argument("--variant", type=int, default=0, help="hobf_conv2d_prepared_ex schedule (0 = automatic)")
 a = ap.parse_args()
 cfg = inputs.CONFIGS[a.config]
 we, wf = cfg.formats[0] if not a.format else tuple(int(v) for v in a.format[1:].split("m"))
@@ -34,7 +35,7 @@ if a.kernel == "tables":
     wt = H.prepare_weights(f, wp, 3, 3, cfg.cin, cfg.cout)
     xr = H.prepare_activations(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, cfg.pad)
     run = lambda: H.conv2d_prepared(f, xr, cfg.n, cfg.h, cfg.w, cfg.cin, wt, 3, 3, cfg.cout,  # noqa: E731
-                                    cfg.stride, cfg.pad)
+                                    cfg.stride, cfg.pad, variant=a.variant)
     G = g["mac_tab"]
 else:
     run = lambda: H.conv2d(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, wp, 3, 3, cfg.cout, cfg.stride, cfg.pad)  # noqa: E731
@@ -55,6 +56,6 @@ ms = float(np.median(ts))
 macs = cfg.macs()
 peak = 148 * 64 * 1.965e9
 print(json.dumps({"config": a.config, "format": f"e{we}m{wf}", "kernel": a.kernel,
-                  "variant": os.environ.get("HOBF_CONV_VARIANT", "default"), "ms": ms,
+                  "variant": a.variant, "ms": ms,
                   "mac_per_s": macs / ms * 1e3, "G": G, "frac": macs * G / 32 / (ms * 1e-3) / peak,
                   "same_as_first": bool(torch.equal(y, y0))}))
