@@ -300,12 +300,71 @@ __global__ void __launch_bounds__(256) pack_t_kernel(const void* __restrict__ sr
   }
 }
 
+// float32 -> planes for the formats of the generated table (we 4-6, wf 2-10): the
+// 32 floats are transposed first and encoded in bitsliced form
+// (hobf::encode_planes_f32: ~3 lop3 per output plane instead of ~20 scalar ops
+// per element), so the kernel moves its bytes at close to HBM speed.
+template <int WE, int WF>
+__global__ void __launch_bounds__(256) pack_f32_bs_kernel(const float* __restrict__ src, int64_t items, int rnd,
+                                                          uint32_t* __restrict__ planes) {
+  constexpr int NB = 3 + WE + WF, NP = (NB + 3) / 4 * 4;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t U[32];
+    const uint4* in = reinterpret_cast<const uint4*>(src + it * 32);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint4 v = __ldg(in + q);
+      U[4 * q] = v.x; U[4 * q + 1] = v.y; U[4 * q + 2] = v.z; U[4 * q + 3] = v.w;
+    }
+    transpose32(U);  // U[k] = bit k of the 32 floats
+    uint32_t P[NP];
+#pragma unroll
+    for (int j = NB; j < NP; j++) P[j] = 0u;
+    hobf::encode_planes_f32<WE, WF>(U, rnd, P);
+    uint4* out = reinterpret_cast<uint4*>(planes + it * NP);
+#pragma unroll
+    for (int q = 0; q < NP / 4; q++) out[q] = make_uint4(P[4 * q], P[4 * q + 1], P[4 * q + 2], P[4 * q + 3]);
+  }
+}
+
+template <int WE, int WF>
+static void go_pack_bs(unsigned b, const void* src, int64_t items, int rnd, uint32_t* planes, cudaStream_t s) {
+  pack_f32_bs_kernel<WE, WF><<<b, 256, 0, s>>>(reinterpret_cast<const float*>(src), items, rnd, planes);
+}
+
+template <int WE>
+static bool pack_bs_we(int wf, unsigned b, const void* src, int64_t items, int rnd, uint32_t* planes,
+                       cudaStream_t s) {
+  switch (wf) {
+    case 2: go_pack_bs<WE, 2>(b, src, items, rnd, planes, s); return true;
+    case 3: go_pack_bs<WE, 3>(b, src, items, rnd, planes, s); return true;
+    case 4: go_pack_bs<WE, 4>(b, src, items, rnd, planes, s); return true;
+    case 5: go_pack_bs<WE, 5>(b, src, items, rnd, planes, s); return true;
+    case 6: go_pack_bs<WE, 6>(b, src, items, rnd, planes, s); return true;
+    case 7: go_pack_bs<WE, 7>(b, src, items, rnd, planes, s); return true;
+    case 8: go_pack_bs<WE, 8>(b, src, items, rnd, planes, s); return true;
+    case 9: go_pack_bs<WE, 9>(b, src, items, rnd, planes, s); return true;
+    case 10: go_pack_bs<WE, 10>(b, src, items, rnd, planes, s); return true;
+  }
+  return false;
+}
+
+static bool launch_pack_bs(int we, int wf, unsigned b, const void* src, int64_t items, int rnd, uint32_t* planes,
+                           cudaStream_t s) {
+  if (we == 4) return pack_bs_we<4>(wf, b, src, items, rnd, planes, s);
+  if (we == 5) return pack_bs_we<5>(wf, b, src, items, rnd, planes, s);
+  if (we == 6) return pack_bs_we<6>(wf, b, src, items, rnd, planes, s);
+  return false;
+}
+
 template <bool FROM_F32>
 static void launch_pack_t(int np, const void* src, int64_t items, int we, int wf, int rnd, uint32_t* planes,
                           cudaStream_t s) {
   int64_t blocks = (items + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   const unsigned b = (unsigned)(blocks < 1 ? 1 : blocks);
+  if (FROM_F32 && launch_pack_bs(we, wf, b, src, items, rnd, planes, s)) return;
   switch (np) {
     case 8: pack_t_kernel<FROM_F32, 8><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
     case 12: pack_t_kernel<FROM_F32, 12><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;

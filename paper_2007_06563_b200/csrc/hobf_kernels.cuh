@@ -116,27 +116,21 @@ __device__ __forceinline__ void store_requant(const uint32_t* acc, const ConvArg
 // bytes (eight 16-byte stores when cout % 4 == 0).  No plane round trip.
 template <class F>
 __device__ __forceinline__ void store_f32(const uint32_t* acc, const ConvArgs& a, int64_t pix, int g) {
-  uint32_t A[32];
-#pragma unroll
-  for (int j = 0; j < 32; j++) A[j] = j < F::NOUT ? acc[j % F::NOUT] : 0u;
-  transpose32(A);  // A[l] = word of lane l
+  uint32_t U[32];
+  decode_planes_f32<F::WE, F::WFO>(acc, U);  // float32 bit planes of the 32 lanes (bitsliced decode)
+  transpose32(U);                            // U[l] = float32 bits of lane l
   float* base = reinterpret_cast<float*>(a.y) + pix * a.cout + 32 * g;
   const int nl = min(32, a.cout - 32 * g);
   if ((a.cout & 3) == 0) {
 #pragma unroll
     for (int q = 0; q < 8; q++) {
       if (4 * q >= nl) break;
-      float4 v;
-      v.x = decode_f32(A[4 * q + 0], F::WE, F::WFO);
-      v.y = decode_f32(A[4 * q + 1], F::WE, F::WFO);
-      v.z = decode_f32(A[4 * q + 2], F::WE, F::WFO);
-      v.w = decode_f32(A[4 * q + 3], F::WE, F::WFO);
-      reinterpret_cast<float4*>(base)[q] = v;
+      reinterpret_cast<uint4*>(base)[q] = make_uint4(U[4 * q], U[4 * q + 1], U[4 * q + 2], U[4 * q + 3]);
     }
   } else {
 #pragma unroll
     for (int l = 0; l < 32; l++)
-      if (l < nl) base[l] = decode_f32(A[l], F::WE, F::WFO);
+      if (l < nl) reinterpret_cast<uint32_t*>(base)[l] = U[l];
   }
 }
 

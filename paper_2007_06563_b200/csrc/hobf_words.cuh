@@ -91,4 +91,92 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Bitsliced float32 <-> F(WE, WF) conversion on 32 lanes at once (the pack
+// kernels and the conv's float32 epilogue): the conversion is done on bit
+// planes with ~3 lop3 per output bit instead of ~20 scalar ops per element.
+// Plane k of U = bit k of the 32 lanes' float32 words (after transpose32).
+
+// Planes of (x + K) mod 2^NO for the NI-bit planes x and a constant K (ripple
+// carry, the constant's bits folded: ~2 lop3 per bit).
+template <int NI, int NO, unsigned K>
+__device__ __forceinline__ void add_const_planes(const uint32_t* x, uint32_t* out) {
+  uint32_t c = 0u;
+#pragma unroll
+  for (int i = 0; i < NO; i++) {
+    const uint32_t xi = i < NI ? x[i] : 0u;
+    const bool k = (K >> i) & 1u;
+    out[i] = k ? ~(xi ^ c) : (xi ^ c);
+    c = k ? (xi | c) : (xi & c);
+  }
+}
+
+// float32 planes U[0..31] -> planes P[0..3+WE+WF-1] of F(WE, WF), rounded at the
+// float's own binade (rnd 0: RNE, 1: RTZ) -- the same function as encode_f32_fast
+// (WE <= 7: every float32 subnormal underflows to a signed zero; overflow -> inf
+// with sign; NaN -> canonical NaN, L5/L6).
+template <int WE, int WF>
+__device__ __forceinline__ void encode_planes_f32(const uint32_t (&U)[32], int rnd, uint32_t* P) {
+  static_assert(WE <= 7 && WF <= 22, "bitsliced encode: WE <= 7, WF <= 22");
+  constexpr int SH = 23 - WF;  // mantissa bits dropped
+  uint32_t sticky = 0u;
+#pragma unroll
+  for (int k = 0; k + 1 < SH; k++) sticky |= U[k];
+  const uint32_t guard = U[SH - 1];
+  const uint32_t inc = rnd == 0 ? (guard & (sticky | U[SH])) : 0u;
+  // increment [kept mantissa (WF) | exponent (8)] by inc; R[WF..WF+7] = rounded exponent
+  uint32_t R[WF + 8];
+  uint32_t c = inc;
+#pragma unroll
+  for (int i = 0; i < WF + 8; i++) {
+    R[i] = U[SH + i] ^ c;
+    c = U[SH + i] & c;
+  }
+  // D = e8r - (127 - bias) as a 9-bit two's complement number: e8r + (512 - OFF)
+  constexpr unsigned OFF = 127u - ((1u << (WE - 1)) - 1u);
+  uint32_t D[9];
+  add_const_planes<8, 9, (512u - OFF) & 511u>(R + WF, D);
+  uint32_t hi = 0u;
+#pragma unroll
+  for (int i = WE; i < 8; i++) hi |= D[i];
+  const uint32_t unf = D[8];
+  const uint32_t ovf = ~D[8] & hi;
+  uint32_t eand = U[23], eor = U[23], mor = 0u;
+#pragma unroll
+  for (int k = 24; k < 31; k++) { eand &= U[k]; eor |= U[k]; }
+#pragma unroll
+  for (int k = 0; k < 23; k++) mor |= U[k];
+  const uint32_t nan = eand & mor;
+  const uint32_t inf = (eand & ~mor) | (ovf & eor & ~eand);
+  const uint32_t normal = eor & ~eand & ~ovf & ~unf;
+#pragma unroll
+  for (int j = 0; j < WF; j++) P[j] = R[j] & normal;
+#pragma unroll
+  for (int j = 0; j < WE; j++) P[WF + j] = D[j] & normal;
+  P[WF + WE] = U[31] & ~nan;
+  P[WF + WE + 1] = normal | nan;
+  P[WF + WE + 2] = inf | nan;
+}
+
+// planes A[0..3+WE+WF-1] of canonical F(WE, WF) words -> float32 planes U[0..31]
+// of their exact values (WE <= 7, WF <= 23): the same function as decode_f32
+// (+-0, +-inf, NaN = 0x7FC00000).
+template <int WE, int WF>
+__device__ __forceinline__ void decode_planes_f32(const uint32_t* A, uint32_t (&U)[32]) {
+  static_assert(WE <= 7 && WF <= 23, "bitsliced decode: WE <= 7, WF <= 23");
+  const uint32_t c0 = A[WF + WE + 1], c1 = A[WF + WE + 2];
+  const uint32_t normal = c0 & ~c1, nan = c0 & c1, spec = c1;  // spec: inf or NaN
+#pragma unroll
+  for (int k = 0; k < 23; k++) U[k] = 0u;
+#pragma unroll
+  for (int i = 0; i < WF; i++) U[23 - WF + i] = A[i] & normal;
+  U[22] |= nan;
+  constexpr unsigned OFF = 127u - ((1u << (WE - 1)) - 1u);
+  uint32_t E[8];
+  add_const_planes<WE, 8, OFF>(A + WF, E);
+#pragma unroll
+  for (int i = 0; i < 8; i++) U[23 + i] = (E[i] & normal) | spec;
+  U[31] = A[WF + WE] & ~nan;
+}
 }  // namespace hobf

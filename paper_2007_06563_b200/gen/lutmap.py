@@ -128,7 +128,10 @@ class Mapping:
         return len(self.luts)
 
 
-def map_aig(aig, outputs: list[int], passes: int = 4, max_cuts: int = 24) -> Mapping:
+def map_aig(aig, outputs: list[int], passes: int = 4, max_cuts: int = 24, resynth: bool = True) -> Mapping:
+    """Map the AIG onto 3-input LUTs (cut enumeration, area flow, exact local area
+    recovery, the absorb post-pass) and, with ``resynth``, restructure the LUT
+    network across the cover (``lutopt.optimize``: exact window resynthesis)."""
     n = aig.n_nodes()
     kind = aig.kind
     cuts: list[list[Cut]] = [None] * n
@@ -256,6 +259,9 @@ def map_aig(aig, outputs: list[int], passes: int = 4, max_cuts: int = 24) -> Map
             c = chosen[v]
             luts.append((v, c.leaves, _full(c.tt, len(c.leaves))))
     luts = absorb_small_luts(luts, outputs)
+    if resynth:
+        from . import lutopt
+        luts = absorb_small_luts(lutopt.optimize(luts, outputs, aig.input_nodes), outputs)
     return Mapping(aig, outputs, luts, chosen)
 
 
