@@ -198,6 +198,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def gpu_index(dist):
+    """One rank per GPU.  With more ranks than GPUs (HOBF_OVERSUBSCRIBE=1 only: a
+    correctness run of the shard / gather path on a 1-GPU box, never a scaling
+    measurement) ranks share devices round-robin."""
+    import torch
+    n = torch.cuda.device_count()
+    if dist.local < n:
+        return dist.local
+    if os.environ.get("HOBF_OVERSUBSCRIBE") != "1":
+        raise SystemExit(f"rank {dist.rank}: LOCAL_RANK {dist.local} but only {n} GPU(s) visible")
+    return dist.local % n
+
+
 # ----------------------------------------------------------------------------- the rank's problem
 
 class Problem:
@@ -269,14 +282,15 @@ def sass_stats(lib_path, fmt_tag, kernel_symbol, g_per_mac):
         return h
 
     whole = hist(ins)
-    best = None
-    for a, s in ins:
+    best, best_d = None, -1.0
+    for a, s in ins:  # the MAC loop: the backward-branch body with >= G LOP3 and the highest LOP3 density
         m = re.search(r"BRA(?:\.U)?\s+(?:!?U?P\d,\s*)?(0x[0-9a-f]+)", s)
         if m and int(m.group(1), 16) < a:
             lo = int(m.group(1), 16)
             body = [(y, x) for y, x in ins if lo <= y <= a]
-            if best is None or len(body) > len(best):
-                best = body
+            nl = sum(1 for _, x in body if op(x).startswith("LOP3"))
+            if g_per_mac and nl >= g_per_mac and nl / len(body) > best_d:
+                best, best_d = body, nl / len(body)
     loop = hist(best) if best else {}
     lop3 = loop.get("LOP3", 0)
     return {"symbol": kernel_symbol, "instructions": len(ins), "LOP3": whole.get("LOP3", 0),
@@ -389,8 +403,8 @@ def run_gpu(a, dist):
     import torch
     from paper_2007_06563_b200 import hobf as H
 
-    torch.cuda.set_device(dist.local)
-    dev = torch.device("cuda", dist.local)
+    dev = torch.device("cuda", gpu_index(dist))
+    torch.cuda.set_device(dev)
     cfg = inputs.CONFIGS[a.config]
     we, wf = fmt_of(cfg, a.format)
     rnd = 0 if a.round == "rne" else 1
@@ -641,6 +655,7 @@ def run_gpu(a, dist):
         "gpu_launches": gpu_launches,
         "clocks": clk,
         "output_sha256": shard.words_sha256(full) if full is not None else None,
+        "oversubscribed": os.environ.get("HOBF_OVERSUBSCRIBE") == "1" and dist.world > torch.cuda.device_count(),
         "f32_epilogue_equals_unpack_f32": f32_consistent,
     }
     if full is not None and not a.no_cpu_baseline:
@@ -660,8 +675,8 @@ def run_sweep(a, dist):
     import torch
     from paper_2007_06563_b200 import hobf as H
 
-    torch.cuda.set_device(dist.local)
-    dev = torch.device("cuda", dist.local)
+    dev = torch.device("cuda", gpu_index(dist))
+    torch.cuda.set_device(dev)
     cfg = inputs.CONFIGS[a.config]
     rnd = 0 if a.round == "rne" else 1
     P = Problem(cfg, dist, a.weak)
@@ -750,7 +765,8 @@ def main(argv=None):
         rc = run_reference(a, dist)
         return rc
     import torch
-    dist.init("nccl" if torch.cuda.is_available() else "gloo")
+    oversub = os.environ.get("HOBF_OVERSUBSCRIBE") == "1"
+    dist.init("nccl" if torch.cuda.is_available() and not oversub else "gloo")
     try:
         if a.sweep:
             return run_sweep(a, dist)

@@ -18,6 +18,7 @@ using hobf::FormatEntry;
 using hobf::xrec_of;
 using hobf::decode_f32;
 using hobf::transpose32;
+using hobf::transpose32_fma;
 
 #define HOBF_DECLARE(TAG)                                                                    \
   cudaError_t hobf_launch_conv_##TAG(const hobf::ConvArgs& a, cudaStream_t s);               \
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict_
 // Used when C is a multiple of 32 (dense rows) and dst is 16-byte aligned.
 template <bool TO_F32, int NP>
 __global__ void __launch_bounds__(256) unpack_t_kernel(const uint32_t* __restrict__ planes, int64_t items, int we,
-                                                       int wf, void* __restrict__ dst) {
+                                                       int wf, void* __restrict__ dst, uint32_t one) {
   const int nb = 3 + we + wf;
   for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
        it += (int64_t)gridDim.x * blockDim.x) {
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(256) unpack_t_kernel(const uint32_t* __restric
 #pragma unroll
     for (int j = 0; j < NP; j++)
       if (j >= nb) A[j] = 0u;  // padding planes are zero anyway; keep the words exact
-    transpose32(A);
+    transpose32_fma(A, one);
     uint4* out = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(dst) + it * 32);
 #pragma unroll
     for (int q = 0; q < 8; q++) {
@@ -250,13 +251,13 @@ static void launch_unpack_t(int np, const uint32_t* planes, int64_t items, int w
   if (blocks > 148 * 32) blocks = 148 * 32;
   const unsigned b = (unsigned)(blocks < 1 ? 1 : blocks);
   switch (np) {
-    case 8: unpack_t_kernel<TO_F32, 8><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
-    case 12: unpack_t_kernel<TO_F32, 12><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
-    case 16: unpack_t_kernel<TO_F32, 16><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
-    case 20: unpack_t_kernel<TO_F32, 20><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
-    case 24: unpack_t_kernel<TO_F32, 24><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
-    case 28: unpack_t_kernel<TO_F32, 28><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
-    default: unpack_t_kernel<TO_F32, 32><<<b, 256, 0, s>>>(planes, items, we, wf, dst); break;
+    case 8: unpack_t_kernel<TO_F32, 8><<<b, 256, 0, s>>>(planes, items, we, wf, dst, 1u); break;
+    case 12: unpack_t_kernel<TO_F32, 12><<<b, 256, 0, s>>>(planes, items, we, wf, dst, 1u); break;
+    case 16: unpack_t_kernel<TO_F32, 16><<<b, 256, 0, s>>>(planes, items, we, wf, dst, 1u); break;
+    case 20: unpack_t_kernel<TO_F32, 20><<<b, 256, 0, s>>>(planes, items, we, wf, dst, 1u); break;
+    case 24: unpack_t_kernel<TO_F32, 24><<<b, 256, 0, s>>>(planes, items, we, wf, dst, 1u); break;
+    case 28: unpack_t_kernel<TO_F32, 28><<<b, 256, 0, s>>>(planes, items, we, wf, dst, 1u); break;
+    default: unpack_t_kernel<TO_F32, 32><<<b, 256, 0, s>>>(planes, items, we, wf, dst, 1u); break;
   }
 }
 
@@ -266,7 +267,7 @@ static void launch_unpack_t(int np, const uint32_t* planes, int64_t items, int w
 // into the group's plane words, stored as NP / 4 128-bit stores.
 template <bool FROM_F32, int NP>
 __global__ void __launch_bounds__(256) pack_t_kernel(const void* __restrict__ src, int64_t items, int we, int wf,
-                                                     int rnd, uint32_t* __restrict__ planes) {
+                                                     int rnd, uint32_t* __restrict__ planes, uint32_t one) {
   const int nb = 3 + we + wf;
   for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
        it += (int64_t)gridDim.x * blockDim.x) {
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(256) pack_t_kernel(const void* __restrict__ sr
         A[l] = canon_word(A[l], we, wf);
       }
     }
-    transpose32(A);  // A[j] = plane j: bit l = field bit j of lane l
+    transpose32_fma(A, one);  // A[j] = plane j: bit l = field bit j of lane l
     uint4* out = reinterpret_cast<uint4*>(planes + it * NP);
 #pragma unroll
     for (int q = 0; q < NP / 4; q++) {
@@ -305,19 +306,28 @@ __global__ void __launch_bounds__(256) pack_t_kernel(const void* __restrict__ sr
 // (hobf::encode_planes_f32: ~3 lop3 per output plane instead of ~20 scalar ops
 // per element), so the kernel moves its bytes at close to HBM speed.
 template <int WE, int WF>
-__global__ void __launch_bounds__(256) pack_f32_bs_kernel(const float* __restrict__ src, int64_t items, int rnd,
-                                                          uint32_t* __restrict__ planes) {
+__global__ void __launch_bounds__(256, 2) pack_f32_bs_kernel(const float* __restrict__ src, int64_t items, int rnd,
+                                                             uint32_t* __restrict__ planes, uint32_t one) {
   constexpr int NB = 3 + WE + WF, NP = (NB + 3) / 4 * 4;
-  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-       it += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // software pipeline over the grid-stride loop: the next group's 128 bytes are in
+  // flight while this group is transposed and encoded
+  uint4 nx[8];
+  auto load = [&](int64_t i) {
+    const uint4* in = reinterpret_cast<const uint4*>(src + i * 32);
+#pragma unroll
+    for (int q = 0; q < 8; q++) nx[q] = __ldg(in + q);
+  };
+  if (it < items) load(it);
+  for (; it < items; it += step) {
     uint32_t U[32];
-    const uint4* in = reinterpret_cast<const uint4*>(src + it * 32);
 #pragma unroll
     for (int q = 0; q < 8; q++) {
-      const uint4 v = __ldg(in + q);
-      U[4 * q] = v.x; U[4 * q + 1] = v.y; U[4 * q + 2] = v.z; U[4 * q + 3] = v.w;
+      U[4 * q] = nx[q].x; U[4 * q + 1] = nx[q].y; U[4 * q + 2] = nx[q].z; U[4 * q + 3] = nx[q].w;
     }
-    transpose32(U);  // U[k] = bit k of the 32 floats
+    if (it + step < items) load(it + step);
+    transpose32_fma(U, one);  // U[k] = bit k of the 32 floats
     uint32_t P[NP];
 #pragma unroll
     for (int j = NB; j < NP; j++) P[j] = 0u;
@@ -329,8 +339,11 @@ __global__ void __launch_bounds__(256) pack_f32_bs_kernel(const float* __restric
 }
 
 template <int WE, int WF>
-static void go_pack_bs(unsigned b, const void* src, int64_t items, int rnd, uint32_t* planes, cudaStream_t s) {
-  pack_f32_bs_kernel<WE, WF><<<b, 256, 0, s>>>(reinterpret_cast<const float*>(src), items, rnd, planes);
+static void go_pack_bs(unsigned, const void* src, int64_t items, int rnd, uint32_t* planes, cudaStream_t s) {
+  // one wave of 2 CTAs per SM, every thread looping over several groups (pipelined)
+  const int64_t b = std::min<int64_t>((items + 255) / 256, 148 * 2);
+  pack_f32_bs_kernel<WE, WF><<<(unsigned)std::max<int64_t>(b, 1), 256, 0, s>>>(reinterpret_cast<const float*>(src),
+                                                                               items, rnd, planes, 1u);
 }
 
 template <int WE>
@@ -366,13 +379,13 @@ static void launch_pack_t(int np, const void* src, int64_t items, int we, int wf
   const unsigned b = (unsigned)(blocks < 1 ? 1 : blocks);
   if (FROM_F32 && launch_pack_bs(we, wf, b, src, items, rnd, planes, s)) return;
   switch (np) {
-    case 8: pack_t_kernel<FROM_F32, 8><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
-    case 12: pack_t_kernel<FROM_F32, 12><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
-    case 16: pack_t_kernel<FROM_F32, 16><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
-    case 20: pack_t_kernel<FROM_F32, 20><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
-    case 24: pack_t_kernel<FROM_F32, 24><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
-    case 28: pack_t_kernel<FROM_F32, 28><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
-    default: pack_t_kernel<FROM_F32, 32><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes); break;
+    case 8: pack_t_kernel<FROM_F32, 8><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes, 1u); break;
+    case 12: pack_t_kernel<FROM_F32, 12><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes, 1u); break;
+    case 16: pack_t_kernel<FROM_F32, 16><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes, 1u); break;
+    case 20: pack_t_kernel<FROM_F32, 20><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes, 1u); break;
+    case 24: pack_t_kernel<FROM_F32, 24><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes, 1u); break;
+    case 28: pack_t_kernel<FROM_F32, 28><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes, 1u); break;
+    default: pack_t_kernel<FROM_F32, 32><<<b, 256, 0, s>>>(src, items, we, wf, rnd, planes, 1u); break;
   }
 }
 
@@ -561,19 +574,32 @@ __device__ __forceinline__ void quantize_row_tile(const float* __restrict__ x, i
     const int qd = threadIdx.x % quads, ix0 = threadIdx.x / quads;
     const float4* __restrict__ src = reinterpret_cast<const float4*>(x + (((int64_t)ni * h + iy) * w) * cin + c0);
     if (ix0 < ppt) {
-      for (int ix = ix0; ix < w; ix += ppt) {
-        const float4 v = __ldg(src + (int64_t)ix * (cin >> 2) + qd);
-        uint32_t* d = srec + (4 * qd) * stride + ix;
-        if (we <= 7) {
-          d[0] = xrec_of(encode_f32_fast(v.x, we, wf, rnd), we, wf);
-          d[stride] = xrec_of(encode_f32_fast(v.y, we, wf, rnd), we, wf);
-          d[2 * stride] = xrec_of(encode_f32_fast(v.z, we, wf, rnd), we, wf);
-          d[3 * stride] = xrec_of(encode_f32_fast(v.w, we, wf, rnd), we, wf);
-        } else {
-          d[0] = xrec_of(encode_f32(v.x, we, wf, rnd), we, wf);
-          d[stride] = xrec_of(encode_f32(v.y, we, wf, rnd), we, wf);
-          d[2 * stride] = xrec_of(encode_f32(v.z, we, wf, rnd), we, wf);
-          d[3 * stride] = xrec_of(encode_f32(v.w, we, wf, rnd), we, wf);
+      // UNR float4 loads of this thread in flight before any encode (the loop is
+      // otherwise one dependent HBM round trip per iteration)
+      constexpr int UNR = 4;
+      for (int ix = ix0; ix < w; ix += UNR * ppt) {
+        float4 v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+          const int xx = ix + u * ppt;
+          v[u] = xx < w ? __ldg(src + (int64_t)xx * (cin >> 2) + qd) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; u++) {
+          const int xx = ix + u * ppt;
+          if (xx >= w) break;
+          uint32_t* d = srec + (4 * qd) * stride + xx;
+          if (we <= 7) {
+            d[0] = xrec_of(encode_f32_fast(v[u].x, we, wf, rnd), we, wf);
+            d[stride] = xrec_of(encode_f32_fast(v[u].y, we, wf, rnd), we, wf);
+            d[2 * stride] = xrec_of(encode_f32_fast(v[u].z, we, wf, rnd), we, wf);
+            d[3 * stride] = xrec_of(encode_f32_fast(v[u].w, we, wf, rnd), we, wf);
+          } else {
+            d[0] = xrec_of(encode_f32(v[u].x, we, wf, rnd), we, wf);
+            d[stride] = xrec_of(encode_f32(v[u].y, we, wf, rnd), we, wf);
+            d[2 * stride] = xrec_of(encode_f32(v[u].z, we, wf, rnd), we, wf);
+            d[3 * stride] = xrec_of(encode_f32(v[u].w, we, wf, rnd), we, wf);
+          }
         }
       }
     }
@@ -616,6 +642,121 @@ __global__ void __launch_bounds__(256) quantize_acts_row_flat_kernel(const float
                       (int)(rest / n) * cc);
     __syncthreads();  // srec is refilled by the next tile
   }
+}
+
+// float32 NHWC -> activation records, bitsliced (the fast path for the formats of
+// the generated table when cin % 32 == 0): one thread per (image, padded row,
+// 32-channel group, padded column), columns fastest.  The thread's 32 channel
+// floats (128 contiguous bytes) are transposed into bit planes, encoded in
+// bitsliced form (encode_planes_f32), the record's table-row field is formed on
+// the planes too (row = frac for a normal x, 2^wF + {0, 1, 2} for zero / inf /
+// NaN), and a second transpose gives the 32 records, stored one per channel row
+// of the [n][c][h+2p][w+2p] layout (consecutive threads = consecutive columns:
+// coalesced).  Padding positions store the +0 record.
+template <int WE, int WF>
+__global__ void __launch_bounds__(256, 2) quantize_acts_bs_kernel(const float* __restrict__ x, int n, int h, int w,
+                                                                  int cin, int pad, int rnd,
+                                                                  uint32_t* __restrict__ rec, uint32_t one) {
+  constexpr int NB = 3 + WE + WF;
+  static_assert(NB <= 20 && WF >= 2, "record layout: word in bits [0, 20), row in [20, 32)");
+  const int Hp = h + 2 * pad, Wp = w + 2 * pad, CG = cin >> 5;
+  const int64_t items = (int64_t)n * Hp * CG * Wp;
+  const uint32_t zero_rec = (1u << WF) << 20;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  // item -> (image, padded row, channel group, padded column), columns fastest;
+  // the next item's 128 bytes are loaded while this one is encoded (pipeline)
+  struct Pos { int ni, iyp, cg, ixp; bool in; };
+  auto pos = [&](int64_t it) {
+    Pos p;
+    p.ixp = (int)(it % Wp);
+    const int64_t r1 = it / Wp;
+    p.cg = (int)(r1 % CG);
+    const int64_t r2 = r1 / CG;
+    p.iyp = (int)(r2 % Hp);
+    p.ni = (int)(r2 / Hp);
+    const int iy = p.iyp - pad, ix = p.ixp - pad;
+    p.in = iy >= 0 && iy < h && ix >= 0 && ix < w;
+    return p;
+  };
+  uint4 nx[8];
+  auto load = [&](const Pos& p) {
+    if (!p.in) return;
+    const uint4* src =
+        reinterpret_cast<const uint4*>(x + (((int64_t)p.ni * h + p.iyp - pad) * w + p.ixp - pad) * cin + 32 * p.cg);
+#pragma unroll
+    for (int q = 0; q < 8; q++) nx[q] = __ldg(src + q);
+  };
+  int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  Pos cur = pos(it < items ? it : 0);
+  if (it < items) load(cur);
+  for (; it < items; it += step) {
+    uint32_t Q[32];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      Q[4 * q] = nx[q].x; Q[4 * q + 1] = nx[q].y; Q[4 * q + 2] = nx[q].z; Q[4 * q + 3] = nx[q].w;
+    }
+    const Pos p = cur;
+    if (it + step < items) {
+      cur = pos(it + step);
+      load(cur);
+    }
+    if (p.in) {
+      transpose32_fma(Q, one);  // Q[k] = bit k of the 32 floats
+      uint32_t P[NB];
+      hobf::encode_planes_f32<WE, WF>(Q, rnd, P);
+      const uint32_t c0 = P[NB - 2], c1 = P[NB - 1];
+#pragma unroll
+      for (int j = 0; j < 32; j++) Q[j] = j < NB ? P[j % NB] : 0u;
+      // table row: frac (normal; canonical specials have frac 0) | 2^wF + {0: zero, 1: inf, 2: NaN}
+#pragma unroll
+      for (int j = 0; j < WF; j++) Q[20 + j] = P[j];
+      Q[20] |= c1 & ~c0;                // inf -> +1
+      Q[21] |= c1 & c0;                 // NaN -> +2
+      Q[20 + WF] = ~(c0 & ~c1);         // not normal -> 2^wF
+      transpose32_fma(Q, one);          // Q[l] = record of channel 32 cg + l
+    } else {
+#pragma unroll
+      for (int l = 0; l < 32; l++) Q[l] = zero_rec;
+    }
+    uint32_t* dst = rec + (((int64_t)p.ni * cin + 32 * p.cg) * Hp + p.iyp) * Wp + p.ixp;
+    const int64_t cstride = (int64_t)Hp * Wp;
+#pragma unroll
+    for (int l = 0; l < 32; l++) dst[l * cstride] = Q[l];
+  }
+}
+
+template <int WE, int WF>
+static void go_qa_bs(const float* x, int n, int h, int w, int cin, int pad, int rnd, uint32_t* rec, cudaStream_t s) {
+  const int64_t items = (int64_t)n * (h + 2 * pad) * (cin >> 5) * (w + 2 * pad);
+  const int64_t blocks = std::min<int64_t>((items + 255) / 256, 148 * 2);  // one wave, pipelined loop
+  quantize_acts_bs_kernel<WE, WF><<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(x, n, h, w, cin, pad, rnd, rec,
+                                                                                        1u);
+}
+
+template <int WE>
+static bool qa_bs_we(int wf, const float* x, int n, int h, int w, int cin, int pad, int rnd, uint32_t* rec,
+                     cudaStream_t s) {
+  switch (wf) {
+    case 2: go_qa_bs<WE, 2>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 3: go_qa_bs<WE, 3>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 4: go_qa_bs<WE, 4>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 5: go_qa_bs<WE, 5>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 6: go_qa_bs<WE, 6>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 7: go_qa_bs<WE, 7>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 8: go_qa_bs<WE, 8>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 9: go_qa_bs<WE, 9>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+    case 10: go_qa_bs<WE, 10>(x, n, h, w, cin, pad, rnd, rec, s); return true;
+  }
+  return false;
+}
+
+static bool launch_qa_bs(int we, int wf, const float* x, int n, int h, int w, int cin, int pad, int rnd,
+                         uint32_t* rec, cudaStream_t s) {
+  if ((cin & 31) != 0 || !aligned16(x) || 3 + we + wf > 20) return false;
+  if (we == 4) return qa_bs_we<4>(wf, x, n, h, w, cin, pad, rnd, rec, s);
+  if (we == 5) return qa_bs_we<5>(wf, x, n, h, w, cin, pad, rnd, rec, s);
+  if (we == 6) return qa_bs_we<6>(wf, x, n, h, w, cin, pad, rnd, rec, s);
+  return false;
 }
 
 // Warp per (weight row, output-channel group, table row): each lane decodes
@@ -1016,6 +1157,11 @@ hobf_status hobf_quantize_activations(hobf_fmt f, const float* d_x, int32_t n, i
   if (!d_x || !d_xrec) return HOBF_EINVAL;
   const int Hp = h + 2 * pad, Wp = w + 2 * pad;
   if ((int64_t)n * Hp > 2147483647LL) return HOBF_EINVAL;
+  if (launch_qa_bs(f.we, f.wf, d_x, n, h, w, cin, pad, f.round, d_xrec, (cudaStream_t)stream)) {
+    if (cudaGetLastError() != cudaSuccess) return HOBF_ECUDA;
+    g_last_launches = 1;
+    return HOBF_OK;
+  }
   const int stride = w | 1;  // odd smem row stride: the transposed writes spread over the banks
   const int cc = (int)std::min<int64_t>(std::min<int64_t>(cin, 256),
                                         std::max<int64_t>(4, (32 * 1024 / 4) / stride) / 4 * 4);

@@ -118,7 +118,7 @@ template <class F>
 __device__ __forceinline__ void store_f32(const uint32_t* acc, const ConvArgs& a, int64_t pix, int g) {
   uint32_t U[32];
   decode_planes_f32<F::WE, F::WFO>(acc, U);  // float32 bit planes of the 32 lanes (bitsliced decode)
-  transpose32(U);                            // U[l] = float32 bits of lane l
+  transpose32_fma(U, (uint32_t)a.one);       // U[l] = float32 bits of lane l
   float* base = reinterpret_cast<float*>(a.y) + pix * a.cout + 32 * g;
   const int nl = min(32, a.cout - 32 * g);
   if ((a.cout & 3) == 0) {
@@ -366,8 +366,11 @@ struct TabTap {
 // runs (latency-bound configs, large tables).
 template <class F, int NT, int MINB, bool KW3, int PD, int RU = 1>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
-  const int g = blockIdx.y;
-  const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // linear grid, output-channel group fastest: the G groups of a pixel tile run
+  // together, so each activation record comes from DRAM once and is reused from L2
+  const int G = (a.cout + 31) >> 5;
+  const int g = (int)(blockIdx.x % G);
+  const int64_t pix = (int64_t)(blockIdx.x / G) * blockDim.x + threadIdx.x;
   if (pix >= (int64_t)a.n * a.ho * a.wo) return;
   const int ox = (int)(pix % a.wo);
   const int oy = (int)((pix / a.wo) % a.ho);
@@ -573,9 +576,10 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_smem_kernel(ConvArgs a) {
   extern __shared__ __align__(128) uint32_t smem_tab[];  // [2][CC][kh*kw][rows][stride]
   __shared__ __align__(8) uint64_t full[2];
   constexpr int S = tab_stride(F::NPT, F::WF), R = F::TAB_ROWS;
-  const int g = blockIdx.y;
+  const int G = (a.cout + 31) >> 5;
+  const int g = (int)(blockIdx.x % G);  // linear grid, output-channel group fastest (see conv_tab_kernel)
   const int64_t npix = (int64_t)a.n * a.ho * a.wo;
-  const int64_t pix_raw = (int64_t)blockIdx.x * NT + threadIdx.x;
+  const int64_t pix_raw = (int64_t)(blockIdx.x / G) * NT + threadIdx.x;
   const bool valid = pix_raw < npix;
   const int64_t pix = valid ? pix_raw : npix - 1;  // idle threads still join the CTA barriers
   const int ox = (int)(pix % a.wo);
@@ -770,7 +774,7 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const int64_t npix = (int64_t)a.n * a.ho * a.wo;
   if (npix == 0) return cudaSuccess;
   const unsigned gy = (unsigned)((a.cout + 31) / 32);
-  auto grid = [&](int threads) { return dim3((unsigned)((npix + threads - 1) / threads), gy); };
+  auto grid = [&](int threads) { return dim3((unsigned)((npix + threads - 1) / threads * gy)); };
   const bool k3 = a.kw == 3;
   int variant = a.variant;
   const int64_t warps = (npix + 31) / 32 * gy;

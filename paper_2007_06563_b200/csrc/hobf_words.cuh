@@ -92,6 +92,41 @@ __device__ __forceinline__ void transpose32(uint32_t (&A)[32]) {
 }
 
 
+// The same transpose with fewer ALU-pipe instructions (the kernels it serves are
+// ALU-issue-bound): the 16- and 8-bit rounds are byte permutes (two PRMT per row
+// pair instead of five shift / logic ops), and in the 4-, 2- and 1-bit rounds the
+// shifts are multiplies on the FMA pipe (x << s = x * 2^s, x >> s = umulhi(x,
+// 2^(32-s))) so only the three lop3 stay on the ALU pipe.  The powers of two
+// must be run-time values (else ptxas turns the multiplies back into shifts):
+// `one` is a kernel argument equal to 1.
+__device__ __forceinline__ void transpose32_fma(uint32_t (&A)[32], uint32_t one) {
+#pragma unroll
+  for (int i = 0; i < 16; i++) {
+    const uint32_t x = A[i], y = A[i + 16];
+    A[i] = __byte_perm(x, y, 0x5410);
+    A[i + 16] = __byte_perm(x, y, 0x7632);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; i++) {
+    if (i & 8) continue;
+    const uint32_t x = A[i], y = A[i + 8];
+    A[i] = __byte_perm(x, y, 0x6240);
+    A[i + 8] = __byte_perm(x, y, 0x7351);
+  }
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const uint32_t m = s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t up = one << s, down = one << (32 - s);  // 2^s, 2^(32-s)
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      if (i & s) continue;
+      const uint32_t t = (__umulhi(A[i], down) ^ A[i + s]) & m;
+      A[i + s] ^= t;
+      A[i] ^= t * up;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Bitsliced float32 <-> F(WE, WF) conversion on 32 lanes at once (the pack
 // kernels and the conv's float32 epilogue): the conversion is done on bit
