@@ -1,0 +1,11 @@
+N="ncu --set full --clock-control none --import-source on"
+cap() {
+  name=$1; k=$2; shift 2
+  timeout 300 $N -k regex:$k --launch-skip 2 --launch-count 1 -o /tmp/$name python tools/ncu_target.py "$@" > gpurun_out/$name.log 2>&1
+  python tools/ncu_summary.py /tmp/$name.ncu-rep "$name: $*" > gpurun_out/$name.txt 2>&1
+  ncu -i /tmp/$name.ncu-rep --page source --csv --print-source sass > /tmp/$name.src.csv 2>/dev/null
+  gzip -c /tmp/$name.src.csv > gpurun_out/$name.src.csv.gz
+  ncu -i /tmp/$name.ncu-rep --page details --csv > gpurun_out/$name.details.csv 2>/dev/null
+}
+cap c3_quant_bs quantize_acts_bs --config C3
+cap mobdw_pack_bs pack_f32_bs --config MOBDW
