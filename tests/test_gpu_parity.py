@@ -743,3 +743,47 @@ def test_conv_kernel_info_reports_the_launch():
     assert k2["variant"] == 5 and k2["threads"] == 32
     kd = H.conv_kernel_info(H.OP_DW, H.Fmt(5, 3, 0), 2, 14, 14, 512, 3, 3, 512, 2, 1)
     assert "conv_dw_kernel" in kd["name"] and kd["local_bytes"] == 0
+
+
+@pytest.mark.parametrize("we,wf", SWEEP)
+def test_bitsliced_quantisers_every_format(we, wf):
+    """The bitsliced float32 encoders (pack_f32_bs_kernel for dense rows,
+    quantize_acts_bs_kernel for cin % 32 == 0) on every format of the sweep, both
+    rounding modes: values spread over the format's whole range and beyond
+    (overflow, underflow, float32 subnormals), exact ties, values one float32 ulp
+    either side of a tie, carries into the next binade, and the specials; words
+    equal the oracle's encode_f32 and the records' row field is the table row."""
+    H = hobf()
+    rng = np.random.default_rng(7000 + we * 16 + wf)
+    bias = (1 << (we - 1)) - 1
+    n = 64 * 1024
+    e = rng.integers(-bias - 4, (1 << we) - bias + 3, n)
+    frac = rng.integers(0, 1 << 23, n)
+    x = np.ldexp(1.0 + frac / 2.0 ** 23, e).astype(np.float32)
+    # exact ties and their float32 neighbours: the bit below the kept fraction set, rest zero
+    tie = np.ldexp(1.0 + (rng.integers(0, 1 << wf, n // 8) * 2 + 1) / 2.0 ** (wf + 1),
+                   rng.integers(-bias, bias, n // 8)).astype(np.float32)
+    x[: n // 8] = tie
+    x[n // 8: n // 4] = np.nextafter(tie, np.float32(np.inf))
+    x[n // 4: 3 * n // 8] = np.nextafter(tie, np.float32(0))
+    x[3 * n // 8: n // 2] = -x[3 * n // 8: n // 2]
+    sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-44, 3.4e38, -3.4e38], np.float32)
+    x[n // 2: n // 2 + sp.size] = sp
+    x = rng.permutation(x)
+    for rnd in (0, 1):
+        exp = oracle.encode_f32(x, we, wf, rnd)
+        planes = H.quantize_pack(we, wf, torch.from_numpy(x.reshape(-1, 64)).cuda(), rnd)
+        got = to_np_words(H.unpack(we, wf, planes, n // 64, 64)).ravel()
+        assert np.array_equal(got, exp), ("pack", rnd, np.nonzero(got != exp)[0][:5])
+        if 3 + we + wf > 20:
+            continue  # records hold the word in 20 bits: no prepared path for this format
+        f = H.Fmt(we, wf, rnd)
+        xa = x.reshape(4, 16, 16, 64)
+        rec = to_np_words(H.quantize_activations(f, torch.from_numpy(xa).cuda(), 1)).reshape(4, 64, 18, 18)
+        inner = rec[:, :, 1:-1, 1:-1].transpose(0, 2, 3, 1).ravel()
+        words = inner & np.uint32((1 << 20) - 1)
+        assert np.array_equal(words, exp), ("records", rnd)
+        exc = (words >> np.uint32(wf + we + 1)) & np.uint32(3)
+        row = np.where(exc == 1, words & np.uint32((1 << wf) - 1), np.uint32(1 << wf) + np.where(exc == 0, 0, exc - 1))
+        assert np.array_equal(inner >> np.uint32(20), row.astype(np.uint32))
+        assert np.all(rec[:, :, 0, :] == np.uint32((1 << wf) << 20)) and np.all(rec[:, :, :, -1] == np.uint32((1 << wf) << 20))
