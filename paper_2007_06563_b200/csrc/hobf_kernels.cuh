@@ -820,7 +820,12 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     const int cfg = (warps >= 148 * 4 * 8 && 12 * blk_bytes <= 216 * 1024) ? 6 : 7;
     auto go = [&](auto kern, int nt, int cc) { return run(a, kern, grid(nt), nt, (size_t)(2 * cc * blk_bytes), s, 7); };
     if (k33) {
-      if (cfg == 6) return go(conv_tab_smem_kernel<F, 128, 6, 1, true>, 128, 1);
+      if (cfg == 6) {
+        // two input channels per staged buffer when the pairs still fit 6 CTAs / SM:
+        // one CTA barrier per two channels
+        if (24 * blk_bytes <= 216 * 1024) return go(conv_tab_smem_kernel<F, 128, 6, 2, true>, 128, 2);
+        return go(conv_tab_smem_kernel<F, 128, 6, 1, true>, 128, 1);
+      }
       return go(conv_tab_smem_kernel<F, 256, 3, 1, true>, 256, 1);
     }
     return go(conv_tab_smem_kernel<F, 256, 4, 1, false>, 256, 1);
