@@ -605,6 +605,11 @@ def run_gpu(a, dist):
     measured_peak = nops / (pe0.elapsed_time(pe1) / 1e3)
     warps = kinfo["blocks"] * ((kinfo["threads"] + 31) // 32)
 
+    # algorithmic bytes of the edge kernel(s): float32 activations in, records / planes out
+    edge_bytes = P.x.nbytes + (4 * n * cin * (h + 2 * pad) * (w + 2 * pad) if use_tab
+                               else 4 * rows_x * ((cin + 31) // 32) * ((f.nin + 3) // 4 * 4))
+    if not f32_out:
+        edge_bytes += 4 * rows_y * ((cout + 31) // 32) * ((f.nout + 3) // 4 * 4) + 4 * rows_y * cout
     if dist.rank != 0:
         return 0
     sass = None
@@ -650,6 +655,17 @@ def run_gpu(a, dist):
                      "conv_ms_median": float(np.median(conv_t)),
                      "mac_per_s_conv_only": macs_step * K / conv_max,
                      "paper_G257_roof_frac": (macs_rank * K / conv_max) / (peak * 32 / 257)},
+        "edge": {  # the step minus the conv: quantise / layout of the activations (plus unpack with --out planes)
+            "ms_per_step": (t_max - conv_max) / K * 1e3,
+            "bytes_per_step": int(edge_bytes),
+            "GBps": edge_bytes / max((t_max - conv_max) / K, 1e-12) / 1e9,
+            "note": "algorithmic bytes (float32 in + records or planes out) / (step - conv) time; includes the "
+                    "launch gap between the two kernels"},
+        "paper_context": {"note": "single CPU core, other hardware (BASELINE.md): context, not a comparison",
+                          "HOBFLOPS9_avx512_mac_per_s": 2e9, "HOBFLOPS9_src": "P:353 (Xeon Gold 5120, 512 lanes)",
+                          "HOBFLOPS16_vs_SoftFP16_avx512": 8.2, "HOBFLOPS16_src": "P:353",
+                          "HOBFLOPS9_neon_mac_per_s": 45e6, "HOBFLOPS9_neon_src": "P:33, P:360 (Cortex-A15)",
+                          "HOBFLOPS8_avx512_gates": {"mul": 53, "add": 204, "src": "P:249"}},
         "sass": sass,
         "e2e": e2e,
         "gpu_launches": gpu_launches,
