@@ -233,7 +233,9 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
  * 2 * kh*kw * (2^wf + 3) * stride * 4 bytes <= 50 KB (wf <= 5 for 3x3), else
  * it falls back to variant 6; 8 = as 7 with one kernel row (3 taps, wf = 6, 7)
  * or one tap (wf = 8, 9) of one input channel per staged buffer (3x3 only,
- * else it falls back to variant 7).
+ * else it falls back to variant 7); 10 / 11 = variant 7 with its CTA shape
+ * forced to 256 threads x 3 per SM / 128 x 6 (variant 7 picks the one that
+ * puts fewer warps on the busiest SM).
  * Variants 3 and 6 need kw == 3 (others fall back to the generic loop).  Every
  * variant
  * runs the same circuit over the same serial (c, kh, kw) order: identical

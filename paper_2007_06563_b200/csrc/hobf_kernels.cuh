@@ -796,7 +796,16 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     // the L1-served kernels: prefetching one tap ahead when the table rows do not stay
     // L1 resident (wF >= 6, measured on C5), or three kernel rows per unrolled loop
     // body at <= 64 registers.
-    variant = warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : units_ok ? 8 : (F::WF >= 6 ? 4 : (k3 ? 6 : 3));
+    // (measured on the strong-split shares of C3 / C4 / C5 / MOB, profiles/r02_shapes_*.txt:
+    // with the tables staged, even 392 warps run better staged than latency-scheduled --
+    // C5 e5m3 at 8 images 0.49 vs 0.35, C3 at 4 images 0.51 vs 0.41)
+    variant = (smem_ok && warps >= 148) ? 7
+              : warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : units_ok ? 8 : (F::WF >= 6 ? 4 : (k3 ? 6 : 3));
+  }
+  int shape = 0;  // variants 10 / 11: variant 7 with the CTA shape forced (256 x 3 / 128 x 6)
+  if (variant >= 10 && variant <= 11) {
+    shape = variant;
+    variant = 7;
   }
   if (variant == 8 && !units_ok) variant = 7;
   if (variant == 7 && !smem_ok) variant = 6;
@@ -813,11 +822,15 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     return cudaGetLastError();
   }
   if (variant == 7) {
-    // 3x3 with >= 8 warps per SMSP of work: 128-thread CTAs x 6 per SM at <= 80
-    // registers (C3 0.846 / C4 0.887 of the roof, vs 0.827 / 0.869 at 8 x 64 registers);
-    // fewer warps (single partial wave): 256-thread CTAs x 3 (MOB 0.785 vs 0.767, C5
-    // +1%); measured, DESIGN.md section 6
-    const int cfg = (warps >= 148 * 4 * 8 && 12 * blk_bytes <= 216 * 1024) ? 6 : 7;
+    // CTA shape: 128 threads x 6 per SM or 256 x 3 (both <= 80 registers, 24 warps per SM),
+    // whichever puts fewer warps on the busiest SM (ceil(CTAs / 148) x warps per CTA),
+    // ties to 256.  Measured (profiles/r02_shapes_*.txt): C3 (44 vs 48 warps) 0.84 vs 0.77,
+    // C4 0.89, MOB / C5 (24 vs 24) 0.78 vs 0.76; strong-split shares: C3 at 8 images
+    // (12 vs 16) 0.70 vs 0.55, C5 at 32 (12 vs 16) 0.74 vs 0.57.
+    auto busiest = [&](int nt) { return ((npix + nt - 1) / nt * gy + 147) / 148 * (nt / 32); };
+    int cfg = (busiest(128) < busiest(256) && 12 * blk_bytes <= 216 * 1024) ? 6 : 7;
+    if (shape == 10) cfg = 7;
+    if (shape == 11 && 12 * blk_bytes <= 216 * 1024) cfg = 6;
     auto go = [&](auto kern, int nt, int cc) { return run(a, kern, grid(nt), nt, (size_t)(2 * cc * blk_bytes), s, 7); };
     if (k33) {
       if (cfg == 6) {

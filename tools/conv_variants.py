@@ -23,8 +23,12 @@ ap.add_argument("--kernel", default="tables")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--round", type=int, default=0)
 ap.add_argument("--variant", type=int, default=0, help="hobf_conv2d_prepared_ex schedule (0 = automatic)")
+ap.add_argument("--n", type=int, default=0, help="batch override (a rank's share under the strong split)")
 a = ap.parse_args()
 cfg = inputs.CONFIGS[a.config]
+if a.n:
+    import dataclasses
+    cfg = dataclasses.replace(cfg, n=a.n)
 we, wf = cfg.formats[0] if not a.format else tuple(int(v) for v in a.format[1:].split("m"))
 f = H.Fmt(we, wf, a.round)
 x, w = inputs.draw(cfg)
@@ -55,7 +59,7 @@ for _ in range(a.reps):
 ms = float(np.median(ts))
 macs = cfg.macs()
 peak = 148 * 64 * 1.965e9
-print(json.dumps({"config": a.config, "format": f"e{we}m{wf}", "kernel": a.kernel,
+print(json.dumps({"config": a.config, "n": cfg.n, "format": f"e{we}m{wf}", "kernel": a.kernel,
                   "variant": a.variant, "ms": ms,
                   "mac_per_s": macs / ms * 1e3, "G": G, "frac": macs * G / 32 / (ms * 1e-3) / peak,
                   "same_as_first": bool(torch.equal(y, y0))}))
