@@ -839,6 +839,7 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
         if (24 * blk_bytes <= 216 * 1024) return go(conv_tab_smem_kernel<F, 128, 6, 2, true>, 128, 2);
         return go(conv_tab_smem_kernel<F, 128, 6, 1, true>, 128, 1);
       }
+      if (12 * blk_bytes <= 216 * 1024) return go(conv_tab_smem_kernel<F, 256, 3, 2, true>, 256, 2);
       return go(conv_tab_smem_kernel<F, 256, 3, 1, true>, 256, 1);
     }
     return go(conv_tab_smem_kernel<F, 256, 4, 1, false>, 256, 1);
