@@ -21,3 +21,7 @@ for n in 2 4; do
   python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $n --steps 3 --warmup 1 --no-e2e --no-sass --no-cpu-baseline > gpurun_out/r02_split_c3_n$n.json 2> gpurun_out/r02_split_c3_n$n.err
   python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29512 bench.py --config C2 --gpus $n --steps 3 --warmup 1 --no-e2e --no-sass --no-cpu-baseline > gpurun_out/r02_split_c2_n$n.json 2> gpurun_out/r02_split_c2_n$n.err
 done
+# shares of C3 / C5 under the strong split (per-GPU work at N = 2, 4, 8), automatic schedule
+for n in 16 8 4; do python tools/conv_variants.py --config C3 --n $n --reps 10 2>&1 | tail -1; done > gpurun_out/r02_shares_c3.txt
+for n in 32 16 8; do python tools/conv_variants.py --config C5 --format e5m3 --n $n --reps 10 2>&1 | tail -1; done > gpurun_out/r02_shares_c5.txt
+for n in 128 64 32; do python tools/conv_variants.py --config C4 --n $n --reps 5 2>&1 | tail -1; done > gpurun_out/r02_shares_c4.txt
