@@ -614,8 +614,10 @@ def run_gpu(a, dist):
         return 0
     sass = None
     if not a.no_sass:
-        tag = f"e{we}m{wf}"
-        sass = sass_stats(H.LIB_PATH, tag, kinfo["name"], G)
+        try:
+            sass = sass_stats(H.LIB_PATH, f"e{we}m{wf}", kinfo["name"], G)
+        except (OSError, subprocess.SubprocessError) as e:  # cuobjdump missing or failing: evidence only
+            sass = {"error": str(e)}
     s0 = P.shard
     line = {
         "metric": METRIC, "value": value, "unit": "MAC/s", "n_gpus": dist.world, "steps": K, "warmup": a.warmup,
