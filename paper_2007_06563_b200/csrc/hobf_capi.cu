@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(256) quantize_acts_row_flat_kernel(const float
 // NaN), and a second transpose gives the 32 records, stored one per channel row
 // of the [n][c][h+2p][w+2p] layout (consecutive threads = consecutive columns:
 // coalesced).  Padding positions store the +0 record.
-template <int WE, int WF>
+template <int WE, int WF, typename IDX>
 __global__ void __launch_bounds__(256, 2) quantize_acts_bs_kernel(const float* __restrict__ x, int n, int h, int w,
                                                                   int cin, int pad, int rnd,
                                                                   uint32_t* __restrict__ rec, uint32_t one) {
@@ -666,14 +666,17 @@ __global__ void __launch_bounds__(256, 2) quantize_acts_bs_kernel(const float* _
   // item -> (image, padded row, channel group, padded column), columns fastest;
   // the next item's 128 bytes are loaded while this one is encoded (pipeline)
   struct Pos { int ni, iyp, cg, ixp; bool in; };
-  auto pos = [&](int64_t it) {
+  // IDX = uint32_t whenever the item count fits (32-bit divisions are a few
+  // instructions; 64-bit ones cost ~80 and were a quarter of the kernel's issue)
+  auto pos = [&](int64_t it64) {
     Pos p;
-    p.ixp = (int)(it % Wp);
-    const int64_t r1 = it / Wp;
-    p.cg = (int)(r1 % CG);
-    const int64_t r2 = r1 / CG;
-    p.iyp = (int)(r2 % Hp);
-    p.ni = (int)(r2 / Hp);
+    const IDX it = (IDX)it64;
+    p.ixp = (int)(it % (IDX)Wp);
+    const IDX r1 = it / (IDX)Wp;
+    p.cg = (int)(r1 % (IDX)CG);
+    const IDX r2 = r1 / (IDX)CG;
+    p.iyp = (int)(r2 % (IDX)Hp);
+    p.ni = (int)(r2 / (IDX)Hp);
     const int iy = p.iyp - pad, ix = p.ixp - pad;
     p.in = iy >= 0 && iy < h && ix >= 0 && ix < w;
     return p;
@@ -729,8 +732,11 @@ template <int WE, int WF>
 static void go_qa_bs(const float* x, int n, int h, int w, int cin, int pad, int rnd, uint32_t* rec, cudaStream_t s) {
   const int64_t items = (int64_t)n * (h + 2 * pad) * (cin >> 5) * (w + 2 * pad);
   const int64_t blocks = std::min<int64_t>((items + 255) / 256, 148 * 2);  // one wave, pipelined loop
-  quantize_acts_bs_kernel<WE, WF><<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(x, n, h, w, cin, pad, rnd, rec,
-                                                                                        1u);
+  const unsigned b = (unsigned)(blocks < 1 ? 1 : blocks);
+  if (items + (int64_t)b * 256 < (int64_t)UINT32_MAX)
+    quantize_acts_bs_kernel<WE, WF, uint32_t><<<b, 256, 0, s>>>(x, n, h, w, cin, pad, rnd, rec, 1u);
+  else
+    quantize_acts_bs_kernel<WE, WF, uint64_t><<<b, 256, 0, s>>>(x, n, h, w, cin, pad, rnd, rec, 1u);
 }
 
 template <int WE>
