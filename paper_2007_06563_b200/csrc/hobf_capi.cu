@@ -319,6 +319,19 @@ __global__ void __launch_bounds__(256, 2) pack_f32_bs_kernel(const float* __rest
 #pragma unroll
     for (int q = 0; q < 8; q++) nx[q] = __ldg(in + q);
   };
+  // the warp's 32 groups are 4 KB of contiguous source: lane 0 also asks L2 for the
+  // block two iterations ahead in one bulk prefetch (whole DRAM rows instead of the
+  // scattered 16-byte pieces the per-lane loads request first)
+  const int lane = threadIdx.x & 31;
+  auto prefetch = [&](int64_t i0) {
+    if (lane == 0 && i0 < items) {
+      const int64_t bytes = std::min<int64_t>(32, items - i0) * 128;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + i0 * 32), "r"((uint32_t)bytes)
+                   : "memory");
+    }
+  };
+  const int64_t w0 = it - lane;  // first group of this warp
+  prefetch(w0 + step);
   if (it < items) load(it);
   for (; it < items; it += step) {
     uint32_t U[32];
@@ -326,6 +339,7 @@ __global__ void __launch_bounds__(256, 2) pack_f32_bs_kernel(const float* __rest
     for (int q = 0; q < 8; q++) {
       U[4 * q] = nx[q].x; U[4 * q + 1] = nx[q].y; U[4 * q + 2] = nx[q].z; U[4 * q + 3] = nx[q].w;
     }
+    prefetch(it - lane + 2 * step);
     if (it + step < items) load(it + step);
     transpose32_fma(U, one);  // U[k] = bit k of the 32 floats
     uint32_t P[NP];
