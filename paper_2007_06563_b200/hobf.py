@@ -441,3 +441,46 @@ class Conv2d:
                        int(self.relu), nxt=F32)
         ho, wo = conv_out_hw(h, w, self.kh, self.kw, self.stride, self.pad)
         return y.reshape(n, ho, wo, self.cout)
+
+
+class Chain:
+    """A chain of conv layers kept in the custom format between layers (the
+    layer-chaining epilogue of P:262): the float32 input is quantised once into the
+    first layer's activation records; every layer but the last re-rounds its
+    outputs (after its ReLU) into the next layer's format and writes the next
+    layer's records directly (HOBF_OUT_NEXT_RECORDS); the last layer writes exact
+    float32 (HOBF_OUT_F32).  Layers are Conv2d objects on the weight-table path
+    with one exponent width and one rounding mode; the result equals
+    oracle.conv_chain.  Marshalling only: every step runs in the library."""
+
+    def __init__(self, layers):
+        if not layers:
+            raise ValueError("empty chain")
+        we, rnd = layers[0].f.we, layers[0].f.round
+        for l in layers:
+            if l.wtab is None:
+                raise ValueError("every layer of a chain needs prepared weight tables (wf <= 10)")
+            if l.f.we != we or l.f.round != rnd:
+                raise ValueError("a chain keeps one exponent width and one rounding mode")
+        for a, b in zip(layers, layers[1:]):
+            if a.cout != b.cin:
+                raise ValueError("channel counts of consecutive layers differ")
+        self.layers = layers
+
+    def __call__(self, x_f32: torch.Tensor) -> torch.Tensor:
+        n, h, w, cin = x_f32.shape
+        first = self.layers[0]
+        if not x_f32.is_cuda:
+            x_f32 = x_f32.to(first.wtab.device)
+        rec = quantize_activations(first.f, x_f32.to(torch.float32).contiguous(), first.pad)
+        for i, l in enumerate(self.layers):
+            ho, wo = conv_out_hw(h, w, l.kh, l.kw, l.stride, l.pad)
+            if i + 1 < len(self.layers):
+                nx = self.layers[i + 1]
+                rec = conv2d_prepared(l.f, rec, n, h, w, l.cin, l.wtab, l.kh, l.kw, l.cout, l.stride, l.pad,
+                                      int(l.relu), nxt=Next(nx.f.wf, records=True, pad=nx.pad))
+            else:
+                y = conv2d_prepared(l.f, rec, n, h, w, l.cin, l.wtab, l.kh, l.kw, l.cout, l.stride, l.pad,
+                                    int(l.relu), nxt=F32)
+            h, w = ho, wo
+        return y.reshape(n, h, w, self.layers[-1].cout)

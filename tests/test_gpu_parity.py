@@ -787,3 +787,26 @@ def test_bitsliced_quantisers_every_format(we, wf):
         row = np.where(exc == 1, words & np.uint32((1 << wf) - 1), np.uint32(1 << wf) + np.where(exc == 0, 0, exc - 1))
         assert np.array_equal(inner >> np.uint32(20), row.astype(np.uint32))
         assert np.all(rec[:, :, 0, :] == np.uint32((1 << wf) << 20)) and np.all(rec[:, :, :, -1] == np.uint32((1 << wf) << 20))
+
+
+@pytest.mark.parametrize("we,wfs,exts,rnd", [(5, (3, 3, 3), (0, 0, 0), 0), (5, (10, 3, 7), (0, 1, 0), 1),
+                                             (4, (3, 5, 2), (0, 0, 1), 0)])
+def test_chain_public_api_vs_oracle(we, wfs, exts, rnd):
+    """hobf.Chain: three layers (stride 1, 2, 1; ReLU on the first two) kept in the
+    custom format between layers (records epilogue), float32 out of the last;
+    equals oracle.conv_chain decoded."""
+    H = hobf()
+    n, h, w, chans = 2, 13, 11, (24, 40, 33, 48)
+    x, _ = inputs.small_case(170 + we, n, h, w, chans[0], chans[1], "normal", 0.5)
+    ws = [inputs.small_case(180 + i, 1, 3, 3, chans[i], chans[i + 1], "normal", 0.3)[1] for i in range(3)]
+    strides, relus = (1, 2, 1), (1, 1, 0)
+    layers = [H.Conv2d(torch.from_numpy(ws[i]).cuda(), H.Fmt(we, wfs[i], rnd, extended=exts[i]), stride=strides[i],
+                       pad=1, relu=bool(relus[i])) for i in range(3)]
+    y = H.Chain(layers)(torch.from_numpy(x).cuda()).cpu().numpy()
+    xq = oracle.encode_f32(x, we, wfs[0], rnd)
+    spec = [(oracle.encode_f32(ws[i], we, wfs[i], rnd), wfs[i], strides[i], 1, relus[i], exts[i]) for i in range(3)]
+    exp_w = oracle.conv_chain(xq, spec, we, rnd)
+    wfo = 2 * wfs[2] + 1 if exts[2] else wfs[2] + 1
+    exp = oracle.decode_f64(exp_w, we, wfo).astype(np.float32)
+    assert y.shape == exp.shape
+    assert np.array_equal(y.view(np.uint32), exp.view(np.uint32))
