@@ -769,6 +769,14 @@ cudaError_t launch_conv(const ConvArgs& a, cudaStream_t s) {
     return run(a, conv_direct_kernel<F>, dim3((unsigned)blocks), threads, 0, s, 0);
 }
 
+// Warps on the busiest SM when CTAs of nt threads run at most 2 per SM (in rounds).
+inline int64_t busiest_2per(int64_t npix, int64_t gy, int nt) {
+  const int64_t blocks = (npix + nt - 1) / nt * gy;
+  return (blocks + 147) / 148 * (nt / 32);
+}
+inline int64_t busiest352(int64_t npix, int64_t gy) { return busiest_2per(npix, gy, 352); }
+inline int64_t busiest256(int64_t npix, int64_t gy) { return busiest_2per(npix, gy, 256); }
+
 template <class F>
 cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const int64_t npix = (int64_t)a.n * a.ho * a.wo;
@@ -817,6 +825,10 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
       // registers, 512-thread CTAs and per-channel staging at 2 CTAs / SM are slower)
       if (ut == 3) return go(conv_tab_smem_kernel<F, 256, 3, 1, true, 3>);
       if (6 * ub <= 216 * 1024) return go(conv_tab_smem_kernel<F, 256, 3, 1, true, 1>);
+      // two CTAs per SM: 352-thread CTAs hold 22 warps per SM, so a layer of up to
+      // 148 x 22 warps (C5: 3136) runs as one wave instead of 1.32 waves of 256-thread CTAs
+      if (busiest352(npix, gy) < busiest256(npix, gy))
+        return run(a, conv_tab_smem_kernel<F, 352, 2, 1, true, 1>, grid(352), 352, (size_t)(2 * ub), s, 8);
       return go(conv_tab_smem_kernel<F, 256, 2, 1, true, 1>);
     }
     return cudaGetLastError();
