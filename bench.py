@@ -49,7 +49,7 @@ L2_BYTES = 126 * 1024 * 1024
 def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=500)  # C3: ~0.6 s of timed steps (>= 0.5 s)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="hobf", choices=["hobf", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(inputs.CONFIGS))
@@ -180,7 +180,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        sm, smax, pw, reasons = [], [], [], set()
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 7:
@@ -190,11 +190,16 @@ class ClockSampler:
                 smax.append(float(p[1]))
             except ValueError:
                 continue
+            try:
+                pw.append(float(p[2]))
+            except ValueError:
+                pass
             for name, v in zip(self.NAMES, p[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
+                "power_w_median": statistics.median(pw) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
