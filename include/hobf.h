@@ -130,7 +130,8 @@ hobf_status hobf_gate_count(hobf_fmt f, int32_t* mac, int32_t* mul, int32_t* add
  * Results are identical to hobf_conv2d.
  *
  * hobf_wtab_words: size in uint32 words of the table buffer for these weights,
- * or -1 if the format has no table kernel (wf > 10, extended class).
+ * or -1 if the format has no table kernel (wf > 10).  Extended-class entries
+ * hold the exact product (2wf+1 fraction bits).
  * Layout: [ceil(cout/32)][cin][kh][kw][2^wf + 3 rows][stride] uint32, where an
  * entry has NPT = roundup(wfo + we + 5, 4) planes and rows are padded to
  * stride = NPT + 4 words when wf <= 7 and NPT/4 is even (conflict-free 128-bit
