@@ -13,7 +13,7 @@ the full-gate kernel (``hobf_conv2d``) against the same words on C3.
 C5 (27 formats x 7.4e9 MACs) is beyond the oracle's budget, so the GPU runs the
 full batch of 64 images (the bench's launch shape) and two whole images --
 the first and the last, 2 x 196 x 256 = 100,352 >= 2^16 complete chains --
-are compared per format, RNE; RTZ on the last image.  ("a seeded
+are compared per format, in both rounding modes.  ("a seeded
 sample of >= 2^16 complete output chains per format".)
 
 Cost on a 16-core host: the oracle runs ~0.3e9 MAC/s, so C4 (2.96e10 MACs) is
@@ -99,7 +99,7 @@ def test_C5_whole_images_every_format(we, wf):
     H = hobf()
     cfg = inputs.CONFIGS["C5"]
     x, w = _c5_inputs()
-    for rnd, imgs in ((0, (0, cfg.n - 1)), (1, (cfg.n - 1,))):
+    for rnd, imgs in ((0, (0, cfg.n - 1)), (1, (0, cfg.n - 1))):
         f = H.Fmt(we, wf, rnd)
         got = gpu_bench_path(x, w, f, cfg)
         for i in imgs:
