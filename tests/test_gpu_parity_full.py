@@ -8,7 +8,9 @@ the output pixels), in both rounding modes, through the launch configuration
 ``prepare_weights`` + ``conv2d_prepared`` (schedule chosen automatically for
 the full batch) + ``unpack``.  ReLU is checked at full size on C3 (the GPU's
 fused ReLU against ``oracle.relu`` of the oracle's chains, ledger L12), and
-the full-gate kernel (``hobf_conv2d``) against the same words on C3.
+the full-gate kernel (``hobf_conv2d``) against the same words on C3; the
+float32 epilogue the bench times (``HOBF_OUT_F32``) is compared bit for bit with
+the oracle's words decoded, on every config.
 
 C5 (27 formats x 7.4e9 MACs) is beyond the oracle's budget, so the GPU runs the
 full batch of 64 images (the bench's launch shape) and two whole images --
@@ -42,14 +44,19 @@ def _cuda():
     yield
 
 
-def gpu_bench_path(x, w, f, cfg, relu=0, n=None):
-    """The bench's step on the device: records, weight tables, conv, unpack to words."""
+def gpu_bench_path(x, w, f, cfg, relu=0, n=None, f32=False):
+    """The bench's step on the device: records, weight tables, conv, unpack to words
+    (f32=True: the conv's float32 epilogue, as bench.py times it)."""
     H = hobf()
     n = x.shape[0] if n is None else n
     xt = torch.from_numpy(x).cuda()
     wp = H.quantize_pack(f.we, f.wf, torch.from_numpy(w.reshape(-1, cfg.cout)).cuda(), f.round)
     tab = H.prepare_weights(f, wp, cfg.kh, cfg.kw, cfg.cin, cfg.cout)
     xr = H.quantize_activations(f, xt, cfg.pad)
+    if f32:
+        y = H.conv2d_prepared(f, xr, n, cfg.h, cfg.w, cfg.cin, tab, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad,
+                              relu, nxt=H.F32)
+        return y.cpu().numpy().reshape(n, cfg.ho, cfg.wo, cfg.cout)
     yp = H.conv2d_prepared(f, xr, n, cfg.h, cfg.w, cfg.cin, tab, cfg.kh, cfg.kw, cfg.cout, cfg.stride, cfg.pad,
                            relu)
     rows = n * cfg.ho * cfg.wo
@@ -80,6 +87,10 @@ def test_config_every_output(name, rnd):
     got = gpu_bench_path(x, w, f, cfg)
     assert got.shape == exp.shape
     assert np.array_equal(got, exp), (name, rnd, int((got != exp).sum()), first_mismatches(got, exp))
+    # the bench's own output: the float32 epilogue, every float's bits = the oracle's word decoded
+    y32 = gpu_bench_path(x, w, f, cfg, f32=True)
+    dec = oracle.decode_f64(exp, we, f.wfo).astype(np.float32)
+    assert np.array_equal(y32.view(np.uint32), dec.view(np.uint32))
     if name == "C3":
         # fused ReLU at full size vs the oracle's ReLU of the same chains (L12)
         got_r = gpu_bench_path(x, w, f, cfg, relu=1)
