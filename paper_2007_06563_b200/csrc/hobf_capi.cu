@@ -742,8 +742,118 @@ __global__ void __launch_bounds__(256, 2) quantize_acts_bs_kernel(const float* _
   }
 }
 
+// float32 -> activation record of F(WE, WF) (word | table row << 20), scalar and
+// with every width a compile-time constant (~20 integer ops): the same function
+// as xrec_of(encode_f32_fast(..)).  The rounding to WF fraction bits is done on
+// the float32 pattern (RNE: + half - 1 + lsb below the cut), so t = [e8 | frac]
+// - (127 - bias) << WF is the format's [E | frac] when 0 <= t < 2^(WE+WF);
+// t < 0 is an underflow (float32 zeros and subnormals included, since the
+// format's emin >= -63 for WE <= 7) -> zero keeping the sign; t >= 2^(WE+WF)
+// is an overflow or a float32 inf -> inf keeping the sign; NaN -> canonical NaN
+// (L5/L6).
+template <int WE, int WF, int RND>
+__device__ __forceinline__ uint32_t qrec_f32(uint32_t u, uint32_t one) {
+  static_assert(WE <= 7 && WF <= 17 && 3 + WE + WF <= 20, "record: word in bits [0, 20)");
+  constexpr int SH = 23 - WF;
+  constexpr int TOP = WE + WF + 1;
+  constexpr uint32_t LO = (uint32_t)(127 - ((1 << (WE - 1)) - 1)) << WF;  // [e8 | frac] of the format's E = 0
+  constexpr uint32_t HI = LO + (1u << (WE + WF));                       // first [e8 | frac] past its range
+  constexpr uint32_t SGN = 1u << (WE + WF);
+  // the shifts are multiplies by run-time powers of two (`one` == 1), so they
+  // issue on the FMA pipe and leave the ALU pipe (the binding one) to the rest
+  const uint32_t ur = RND == 0 ? u + ((1u << (SH - 1)) - 1u) + (__umulhi(u, one << (32 - SH)) & 1u) : u;
+  const uint32_t m = __umulhi(ur * (one << 1), one << (31 - SH));  // (ur & 0x7fffffff) >> SH = [e8r | frac]
+  const uint32_t tt = m + ((1u << TOP) - LO);                     // exc 01 | E | frac (when LO <= m < HI)
+  const uint32_t us = __umulhi(u, one << (WE + WF + 1));         // the sign lands on bit WE + WF
+  const uint32_t nrec = ((tt & ((1u << WF) - 1u)) * (one << 20) + tt) | (us & SGN);
+  const uint32_t zrec = (us & SGN) | ((1u << WF) << 20);
+  const uint32_t irec = (us & SGN) | (2u << TOP) | (((1u << WF) + 1u) << 20);
+  constexpr uint32_t qnan = (3u << TOP) | (((1u << WF) + 2u) << 20);
+  const uint32_t r = m < LO ? zrec : (m >= HI ? irec : nrec);
+  return u * (one << 1) > 0xFF000000u ? qnan : r;
+}
+
+// float32 NHWC -> activation records (cin % 16 == 0, the generated formats), no
+// shared memory: one CTA per (image, padded row); a warp's unit is 8 padded
+// columns x 16 channels, lane = (column cl, channel quad q): one float4 load per
+// lane (8 x 64 contiguous bytes per warp), 4 records encoded (qrec_f32), and 4
+// stores -- for each j the warp writes 8 consecutive columns of the 4 channel rows
+// 4q + j (32-byte segments of the [n][c][h+2p][w+2p] layout).  Padding columns /
+// rows store the +0 record.  Up to 4 units' loads are in flight per thread.
+// (A one-wave grid with the units spread over all warps, to remove the CTA tail
+// wave, measured slower: C3 18.4 -> 21.0 us, C4 55 -> 86 us.)
+template <int WE, int WF, int RND>
+__global__ void __launch_bounds__(256, 6) quantize_acts_direct_kernel(const float* __restrict__ x, int h, int w,
+                                                                      int cin, int pad, uint32_t* __restrict__ rec,
+                                                                      uint32_t one) {
+  constexpr int MAXU = 4;
+  const int Hp = h + 2 * pad, Wp = w + 2 * pad;
+  const int iyp = blockIdx.x % Hp, ni = blockIdx.x / Hp;
+  const int iy = iyp - pad;
+  const bool row_in = iy >= 0 && iy < h;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cl = lane & 7, q = lane >> 3;
+  const int G16 = cin >> 4, XB = (Wp + 7) >> 3;
+  const int units = G16 * XB;
+  // u -> (column block, 16-channel group) by a multiply-high (exact: G16^2 * XB < 2^32)
+  const uint32_t magic = G16 == 1 ? 0u : 0xFFFFFFFFu / (uint32_t)G16 + 1u;
+  auto split = [&](int u, int& xb, int& g) {
+    xb = G16 == 1 ? u : (int)__umulhi((uint32_t)u, magic);
+    g = u - xb * G16;
+  };
+  const float* __restrict__ xrow = x + ((int64_t)ni * h + (row_in ? iy : 0)) * w * cin + 4 * q;
+  uint32_t* __restrict__ dst = rec + ((int64_t)ni * cin * Hp + iyp) * Wp + cl;
+  const int64_t cs = (int64_t)Hp * Wp;
+  for (int u0 = warp; u0 < units; u0 += 8 * MAXU) {
+    float4 v[MAXU];
+#pragma unroll
+    for (int k = 0; k < MAXU; k++) {
+      const int u = u0 + 8 * k;
+      int xb, g;
+      split(u, xb, g);
+      const int ix = 8 * xb + cl - pad;
+      v[k] = (u < units && row_in && ix >= 0 && ix < w)
+                 ? __ldg(reinterpret_cast<const float4*>(xrow + (int64_t)ix * cin + 16 * g))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < MAXU; k++) {
+      const int u = u0 + 8 * k;
+      int xb, g;
+      split(u, xb, g);
+      const int ixp = 8 * xb + cl;
+      // padding positions hold +0.0f, whose record is the +0 record: no branch
+      const uint32_t r0 = qrec_f32<WE, WF, RND>(__float_as_uint(v[k].x), one);
+      const uint32_t r1 = qrec_f32<WE, WF, RND>(__float_as_uint(v[k].y), one);
+      const uint32_t r2 = qrec_f32<WE, WF, RND>(__float_as_uint(v[k].z), one);
+      const uint32_t r3 = qrec_f32<WE, WF, RND>(__float_as_uint(v[k].w), one);
+      if (u < units && ixp < Wp) {
+        uint32_t* d = dst + (16 * g + 4 * q) * cs + 8 * xb;
+        d[0] = r0;
+        d[cs] = r1;
+        d[2 * cs] = r2;
+        d[3 * cs] = r3;
+      }
+    }
+  }
+}
+
+template <int WE, int WF, int RND>
+static bool go_qa_tile(const float* x, int n, int h, int w, int cin, int pad, uint32_t* rec, cudaStream_t s) {
+  const int64_t ctas = (int64_t)n * (h + 2 * pad);
+  const int64_t g16 = cin >> 4, xb = (w + 2 * pad + 7) >> 3;
+  if ((cin & 15) != 0 || ctas > 2147483647LL || g16 * g16 * xb >= (1LL << 32) || g16 * xb > 2147483647LL - 256)
+    return false;
+  quantize_acts_direct_kernel<WE, WF, RND><<<(unsigned)ctas, 256, 0, s>>>(x, h, w, cin, pad, rec, 1u);
+  return true;
+}
+
 template <int WE, int WF>
 static void go_qa_bs(const float* x, int n, int h, int w, int cin, int pad, int rnd, uint32_t* rec, cudaStream_t s) {
+#ifndef HOBF_NO_QA_TILE  // (A/B builds of the development tools only)
+  if (rnd == 0 ? go_qa_tile<WE, WF, 0>(x, n, h, w, cin, pad, rec, s) : go_qa_tile<WE, WF, 1>(x, n, h, w, cin, pad, rec, s))
+    return;
+#endif
   const int64_t items = (int64_t)n * (h + 2 * pad) * (cin >> 5) * (w + 2 * pad);
   const int64_t blocks = std::min<int64_t>((items + 255) / 256, 148 * 2);  // one wave, pipelined loop
   const unsigned b = (unsigned)(blocks < 1 ? 1 : blocks);
