@@ -255,11 +255,15 @@ def fp_mul(g: AIG, A: FP, B: FP, wfo: int, rnd: int):
         rounded, rc = kept, FALSE
     frac = rounded[:wfo]                       # if rc, these are all zero already
 
-    # exponent: Ea + Eb - bias + top + rc in wE+2 bits (two's complement)
+    # exponent: Ea + Eb - bias + top + rc in wE+2 bits (two's complement).  top
+    # and rc are never both 1 (a satisfiability don't-care the AIG cannot see): a
+    # rounding carry needs the wfo+1 kept bits all ones and the guard set, i.e.
+    # P >= 2^(2wF+2) - 2^(2wF-wfo) when top = 1, above the largest product
+    # (2^(wF+1) - 1)^2 for every wfo >= wF -- so one carry-in (top | rc) replaces
+    # the separate round-carry incrementer (e5m2 mul 66 -> 56 lop3).
     EW = we + 2
-    s1 = ripple_add(g, A.exp, B.exp, top, width=EW)
-    s2 = ripple_add(g, s1, const_bits((1 << EW) - bias(we), EW), FALSE, width=EW)
-    E, _ = increment(g, s2, rc, width=EW)
+    s1 = ripple_add(g, A.exp, B.exp, g.OR(top, rc), width=EW)
+    E = ripple_add(g, s1, const_bits((1 << EW) - bias(we), EW), FALSE, width=EW)
     unf = E[EW - 1]
     ovf = g.AND(g.NOT(E[EW - 1]), E[EW - 2])   # E >= 2^wE (E < 2^(wE+1) always)
 

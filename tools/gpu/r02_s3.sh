@@ -1,0 +1,11 @@
+(time python -m pytest tests -m gpu -x -q) > gpurun_out/s3_gputest.log 2>&1; tail -3 gpurun_out/s3_gputest.log
+python bench.py > gpurun_out/s3_bench_c3.json 2>gpurun_out/s3_bench_c3.err
+B="python bench.py --no-cpu-baseline"
+$B --kernel gates --steps 50 > gpurun_out/s3_bench_c3_gates.json 2>&1
+$B --config C4 --steps 10 --kernel gates > gpurun_out/s3_bench_c4_gates.json 2>&1
+$B --config MOBDW --steps 50 > gpurun_out/s3_bench_mobdw.json 2>&1
+$B --config C4 --steps 20 > gpurun_out/s3_bench_c4.json 2>&1
+python tools/edge_bench.py --configs C3,C4,C5,MOB,MOBDW > gpurun_out/s3_edge.txt 2>&1
+for f in gpurun_out/s3_bench_*.json; do python -c "
+import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); r=d['roofline']
+print('$f', '%.4g'%d['value'], d['ms_per_step'], r['frac'], r.get('gates_per_32lane_mac'))"; done
