@@ -85,6 +85,30 @@ def test_mul_exhaustive(we, wf, rnd):
     _check(c, m, [A, B], oracle.mul(A, B, we, wf, wf + 1, rnd))
 
 
+def test_mul_normalise_and_round_carries_exclusive():
+    """fpgen.fp_mul adds the normalisation carry (product >= 2) and the rounding
+    carry through ONE exponent carry-in (top | rc), which is exact only if they
+    are never both 1.  Brute force over every significand pair for wF <= 7 and
+    every rounding width wF <= wfo <= 2wF (RNE: the only mode with a carry), and
+    the closed form (largest product (2^(wF+1) - 1)^2 below the carry threshold
+    2^(2wF+2) - 2^(2wF-wfo)) for every wF <= 23."""
+    for wf in range(1, 8):
+        m = np.arange(1 << wf, 1 << (wf + 1), dtype=np.int64)
+        P = np.multiply.outer(m, m).ravel()
+        top = P >= (1 << (2 * wf + 1))
+        for wfo in range(wf, 2 * wf + 1):
+            N = np.where(top, P, P << 1)                       # leading one at bit 2wF+1
+            lo = 2 * wf + 1 - wfo                              # bits below the kept wfo+1
+            kept, rem = N >> lo, N & ((1 << lo) - 1)
+            half = 1 << (lo - 1)
+            up = (rem > half) | ((rem == half) & ((kept & 1) == 1))
+            rc = (kept + up) >> (wfo + 1)                      # rounding carried out of the kept bits
+            assert not np.any(top & (rc == 1)), (wf, wfo)
+    for wf in range(1, 24):
+        for wfo in range(wf, 2 * wf + 1):
+            assert ((1 << (wf + 1)) - 1) ** 2 < (1 << (2 * wf + 2)) - (1 << (2 * wf - wfo))
+
+
 @pytest.mark.parametrize("we,w", [(5, 4), (4, 4), (5, 3), (6, 3)])
 @pytest.mark.parametrize("rnd", [0, 1])
 def test_add_exhaustive(we, w, rnd):
