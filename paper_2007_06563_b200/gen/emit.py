@@ -18,7 +18,7 @@ import sys
 import time
 from concurrent.futures import ProcessPoolExecutor
 
-from . import fpgen
+from . import fpgen, sweep
 from .lutmap import map_aig
 
 RND_NAME = {0: "rne", 1: "rtz"}
@@ -65,6 +65,12 @@ def mapping_to_cuda(circuit, mapping, fname: str, out_arg: str, extra_doc: str =
         lines.append(f"  const uint32_t t{v} = hobf_lop3<0x{tt:02x}>({ops[2]}, {ops[1]}, {ops[0]});")
         expr[v] = f"t{v}"
         n_ops += 1
+    # inputs the network never reads (a plane the SDC sweep found equal to another) are not loaded
+    used = set()
+    for v, leaves, tt in mapping.luts:
+        used.update(leaves)
+    used.update(o >> 1 for o in circuit.outputs)
+    loads = [ld for ld, node in zip(loads, g.input_nodes) if node in used]
     outs = []
     for i, o in enumerate(circuit.outputs):
         v, c = o >> 1, o & 1
@@ -96,14 +102,20 @@ def gen_format(we: int, wf: int, rnd: int, ext: int = 0) -> dict:
     wfo = 2 * wf + 1 if ext else wf + 1
     nin, nout = 3 + we + wf, 3 + we + wfo
     mac = fpgen.build_mac(we, wf, wfo, rnd)
-    mm = map_aig(mac.g, mac.outputs)
     mul = fpgen.build_mul(we, wf, wfo, rnd)
-    mmul = map_aig(mul.g, mul.outputs)
     add = fpgen.build_add(we, wfo, rnd)
+    mtab = fpgen.build_mac_tab(we, wf, rnd, wfo)
+    if not ext:  # merge nodes equal on the valid input space (sweep.py: cached, proved exhaustively)
+        cache = sweep.load_cache()
+        mac = sweep.reduce("mac", mac, we, wf, rnd, wfo, cache)
+        mul = sweep.reduce("mul", mul, we, wf, rnd, wfo, cache)
+        add = sweep.reduce("add", add, we, wf, rnd, wfo, cache)
+        mtab = sweep.reduce("mac_tab", mtab, we, wf, rnd, wfo, cache)
+    mm = map_aig(mac.g, mac.outputs)
+    mmul = map_aig(mul.g, mul.outputs)
     madd = map_aig(add.g, add.outputs)
     relu = fpgen.build_relu(we, wfo)
     mrelu = map_aig(relu.g, relu.outputs)
-    mtab = fpgen.build_mac_tab(we, wf, rnd, wfo)
     mmtab = map_aig(mtab.g, mtab.outputs)
     tw = fpgen.tab_entry_width(we, wf, wfo)
     tag = f"e{we}m{wf}{'x' if ext else ''}_{RND_NAME[rnd]}"

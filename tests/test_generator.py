@@ -340,3 +340,71 @@ def test_absorb_post_pass_preserves_function_and_never_adds_luts():
         got = lutmap.simulate_mapping(m, words, np)
         for r, o in zip(ref, got):
             assert np.array_equal(r, o), trial
+
+
+# ----------------------------------------------------------------------------- SDC sweep (gen/sweep.py)
+
+from paper_2007_06563_b200.gen import sweep  # noqa: E402
+
+
+@pytest.mark.parametrize("we,wf", [(5, 3), (4, 3), (5, 6), (6, 2)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_sweep_table_entries_match_tabref(we, wf, rnd):
+    """The generator's statement of the weight-table entry (the valid input space of
+    the swept mac_tab circuit) equals tests/tabref.py on every (weight, row)."""
+    w = canon_words(we, wf)
+    r = np.arange((1 << wf) + 3)
+    W, R = np.meshgrid(w, r, indexing="ij")
+    for wfo in (wf + 1, 2 * wf + 1):
+        got = sweep.tab_entry(W.ravel(), R.ravel(), we, wf, wfo, rnd)
+        assert np.array_equal(got.astype(np.uint32), tabref.entries(W.ravel(), R.ravel(), we, wf, rnd, wfo))
+
+
+def test_sweep_canonical_words_match_pyref():
+    for we, wf in [(4, 3), (5, 2), (6, 4)]:
+        assert sorted(sweep.canonical_words(we, wf).tolist()) == sorted(pyref.canonical_words(we, wf))
+
+
+@pytest.mark.parametrize("kind,we,wf,rnd", [("mac_tab", 4, 3, 0), ("mac_tab", 5, 2, 1), ("mac", 4, 3, 1),
+                                            ("mul", 5, 2, 0), ("add", 4, 2, 0)])
+def test_sweep_cache_reproved(kind, we, wf, rnd):
+    """The cached merges of a circuit re-proved here on its whole valid input space,
+    and the cache key matches the circuit the generator builds today (so the
+    emitted code is the swept circuit)."""
+    c = sweep.BUILDERS[kind](we, wf, rnd)
+    ent = sweep.load_cache()[c.name]
+    assert ent["key"] == sweep.structure_key(c) and ent["merges"]
+    new = sweep.apply_merges(c, [tuple(m) for m in ent["merges"]])
+    assert sweep.prove(c, new, sweep.space_of(kind, c, we, wf, rnd, wf + 1))
+    assert lutmap.map_aig(new.g, new.outputs).n_luts < lutmap.map_aig(c.g, c.outputs).n_luts
+
+
+def test_sweep_merges_found_from_scratch_e4m2():
+    """Signatures + rebuild + proof from scratch on a small table MAC (e4m2)."""
+    c = fpgen.build_mac_tab(4, 2, 0)
+    space = sweep.space_of("mac_tab", c, 4, 2, 0, 3)
+    merges = sweep.find_merges(c, space)
+    assert merges and sweep.prove(c, sweep.apply_merges(c, merges), space)
+    # and a wrong merge is caught by the proof: a node claimed equal to constant false
+    v = next(v for v in range(c.g.n_nodes()) if c.g.kind[v] == "and" and v not in {m[0] for m in merges}
+             and any(o >> 1 == v for o in c.outputs))
+    assert not sweep.prove(c, sweep.apply_merges(c, merges + [(v, 0, 0)]), space)
+
+
+def test_mac_tab_swept_exhaustive_relaxed_acc_e4m3():
+    """The emitted (swept) e4m3 table MAC over every 7th block of 256 accumulator
+    patterns (the relaxed form: all 2^11 are covered, merged or not, by
+    test_sweep_cache_reproved) and every canonical (x, w) pair: equals the oracle
+    after canonicalisation."""
+    we, wf, rnd = 4, 3, 0
+    c = sweep.reduce("mac_tab", fpgen.build_mac_tab(we, wf, rnd), we, wf, rnd, wf + 1)
+    m = lutmap.map_aig(c.g, c.outputs)
+    xi = canon_words(we, wf)
+    X, W = np.meshgrid(xi, xi, indexing="ij")
+    X, W = X.ravel(), W.ravel()
+    for a0 in range(0, 1 << (3 + we + wf + 1), 256 * 7):
+        acc = np.arange(a0, a0 + 256, dtype=np.uint32)
+        A = np.repeat(acc, X.size)
+        XX, WW = np.tile(X, acc.size), np.tile(W, acc.size)
+        exp = oracle.mac(tabref.canon(A, we, wf + 1), XX, WW, we, wf, wf + 1, rnd)
+        _check(c, m, tabref.circuit_inputs(A, XX, WW, we, wf, rnd), exp, lambda v: tabref.canon(v, we, wf + 1))
