@@ -1,6 +1,6 @@
 # round-2 final refresh (one B200): bench lines, strong-split correctness runs,
 # launch lists and ncu --set full captures of the kernels that changed.
-O=gpurun_out/fin; mkdir -p $O
+O=gpurun_out/fin2; mkdir -p $O
 B="python bench.py"
 $B > $O/r02_bench_c3.json 2> $O/r02_bench_c3.err
 $B --impl reference > $O/r02_bench_c3_reference_arm.json 2>&1
