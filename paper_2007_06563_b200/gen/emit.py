@@ -111,6 +111,8 @@ def gen_format(we: int, wf: int, rnd: int, ext: int = 0) -> dict:
         mul = sweep.reduce("mul", mul, we, wf, rnd, wfo, cache)
         add = sweep.reduce("add", add, we, wf, rnd, wfo, cache)
         mtab = sweep.reduce("mac_tab", mtab, we, wf, rnd, wfo, cache)
+    else:        # extended-class table MACs: GPU-proved merges only (tools/sweep_gpu.py)
+        mtab = sweep.reduce("mac_tab", mtab, we, wf, rnd, wfo, sweep.load_cache(), compute=False)
     mm = map_aig(mac.g, mac.outputs)
     mmul = map_aig(mul.g, mul.outputs)
     madd = map_aig(add.g, add.outputs)

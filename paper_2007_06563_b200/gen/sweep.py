@@ -19,7 +19,9 @@ then compared with the original's on the whole valid space -- that comparison,
 not the signatures, is the proof.  The merge lists are cached in
 ``sweep_cache.json`` (keyed by a structural hash of the AIG), so a build applies
 them without re-simulating; ``python -m paper_2007_06563_b200.gen.sweep``
-recomputes and re-proves the cache.
+recomputes and re-proves the cache.  Entries marked ``"proved": "gpu-exhaustive"``
+(the wider table MACs, up to ~3e14 vectors) were proved by ``tools/sweep_gpu.py``,
+which runs the original and the swept networks on every valid input on the B200.
 """
 from __future__ import annotations
 
@@ -290,15 +292,17 @@ def load_cache():
         return {}
 
 
-def reduce(kind: str, circuit, we: int, wf: int, rnd: int, wfo: int, cache=None):
+def reduce(kind: str, circuit, we: int, wf: int, rnd: int, wfo: int, cache=None, compute: bool = True):
     """The swept circuit (merges from the cache when its structure key matches,
-    else found and proved here), or the circuit unchanged when its valid space is
-    not enumerable."""
+    else -- with ``compute`` -- found and proved here), or the circuit unchanged
+    when its valid space is not enumerable."""
     cache = load_cache() if cache is None else cache
     key = structure_key(circuit)
     ent = cache.get(circuit.name)
     if ent is not None and ent.get("key") == key:
         return apply_merges(circuit, [tuple(m) for m in ent["merges"]])
+    if not compute:
+        return circuit
     space = space_of(kind, circuit, we, wf, rnd, wfo)
     if space is None:
         return circuit
@@ -344,7 +348,8 @@ def main():
     from concurrent.futures import ProcessPoolExecutor
     t0 = time.time()
     jobs = list(_targets())
-    cache = {}
+    # keep the GPU-proved entries (tools/sweep_gpu.py) whose circuit is unchanged
+    cache = {k: v for k, v in load_cache().items() if v.get("proved") == "gpu-exhaustive"}
     with ProcessPoolExecutor() as ex:
         for r in ex.map(_one, jobs):
             if r is None:
