@@ -408,3 +408,13 @@ def test_mac_tab_swept_exhaustive_relaxed_acc_e4m3():
         XX, WW = np.tile(X, acc.size), np.tile(W, acc.size)
         exp = oracle.mac(tabref.canon(A, we, wf + 1), XX, WW, we, wf, wf + 1, rnd)
         _check(c, m, tabref.circuit_inputs(A, XX, WW, we, wf, rnd), exp, lambda v: tabref.canon(v, we, wf + 1))
+
+
+def test_sweep_cache_holds_only_proved_merges():
+    """Every cached merge list was proved on its circuit's whole valid input space
+    (CPU: gen/sweep.py; GPU: tools/sweep_gpu.py, every valid input on the B200)."""
+    cache = sweep.load_cache()
+    assert cache
+    for name, ent in cache.items():
+        assert ent.get("proved") in (True, "gpu-exhaustive"), name
+        assert ent["vectors"] > 0 and ent["key"]
