@@ -236,7 +236,14 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
  * or one tap (wf = 8, 9) of one input channel per staged buffer (3x3 only,
  * else it falls back to variant 7); 10 / 11 = variant 7 with its CTA shape
  * forced to 256 threads x 3 per SM / 128 x 6 (variant 7 picks the one that
- * puts fewer warps on the busiest SM).
+ * puts fewer warps on the busiest SM); 12 = variant 4 on a fractional wave
+ * (the float32 epilogue, cout % 32 == 0, more 128-pixel units than resident
+ * CTAs but at most 1.5 waves): one cooperative CTA per resident slot, each
+ * running its own unit plus one of S <= 16 consecutive tap segments of a unit
+ * past the wave, the segment accumulators handed on through the units' own
+ * float32 output slots (zeroed first, one cudaMemsetAsync) -- the automatic
+ * choice where variant 4 would be; otherwise it runs as variant 4.  Variant 12
+ * launches the conv through cudaLaunchCooperativeKernel.
  * Variants 3 and 6 need kw == 3 (others fall back to the generic loop).  Every
  * variant
  * runs the same circuit over the same serial (c, kh, kw) order: identical

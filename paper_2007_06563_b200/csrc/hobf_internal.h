@@ -30,6 +30,7 @@ struct ConvArgs {
   unsigned two;        // always 2 (see bit01)
   unsigned row_mul;    // 2^12: IMAD.HI(rec, row_mul) = rec >> 20 (table row of an activation record)
   unsigned lift[32];   // lift[j] = 2^(31-j), runtime values so the multiplies stay IMADs
+  int split_e, split_s, split_l;  // variant 12 (fractional wave): extra units, segments per unit, taps per segment
   LaunchInfo* info;    // non-null: record the chosen kernel and launch shape, launch nothing
 };
 

@@ -502,6 +502,210 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Fractional-wave schedule of the L1-served kernel (variant 12, the float32
+// epilogue): U work units (CTA tiles of 128 pixels x one Cout group) on W < U
+// co-resident workers.  Run as variant 4, the E = U - W units past the wave
+// would form a second, nearly empty wave that takes a whole chain's time at a
+// few warps per SM (C5, wF = 10: 784 units on 740 slots).  Here every worker
+// runs one unit (unit b) and, for E * S of them, one of S consecutive tap
+// segments of an extra unit: such a worker does its own taps [0, sL),
+// then segment s of an extra unit of its own Cout group (taps [sL, (s+1)L), the
+// last segment to the end), then its own taps [sL, taps).  Segment s - 1 is done by the time
+// segment s starts (both workers have run sL taps), so the chain of every
+// extra unit moves through the S workers in its serial (c, kh, kw) order
+// (L10): the same chain, the same result as one thread running it.
+// Hand-off: the segment's accumulator planes are stored in the producing
+// thread's own float32 output slot of the extra unit (32 words; NOUT <= 31),
+// then a token (segment index) in the slot's word 31 after a fence; the next
+// segment's thread spins on that word (acquire) and reads the planes through
+// L2.  The host zeroes the extra units' slots before the launch, and the last
+// segment overwrites them with the unit's float32 outputs.  Each worker's own
+// accumulator waits in its own output slot during the extra segment (one
+// accumulator in registers).  The launch is cooperative (every worker
+// resident), so a waiting worker never holds a slot its producer needs.
+// ---------------------------------------------------------------------------
+template <class F>
+__device__ __forceinline__ void tab_span(uint32_t (&acc)[F::NOUT], const ConvArgs& a, const uint32_t* __restrict__ rbase,
+                                         const uint32_t* __restrict__ tbase, int t0, int t1) {
+  if (t0 >= t1) return;
+  const int Wp = a.w + 2 * a.pad;
+  const int64_t cstride = (int64_t)(a.h + 2 * a.pad) * Wp;
+  const int64_t tstride = (int64_t)F::TAB_ROWS * tab_stride(F::NPT, F::WF);
+  const int kk = a.kh * a.kw;
+  auto at = [&](int t) {
+    TapIter it;
+    it.c = t / kk;
+    const int r = t - it.c * kk;
+    it.kh = r / a.kw;
+    it.kw = r - it.kh * a.kw;
+    return it;
+  };
+  // one tap's operands in flight while the previous tap's MAC runs (variant 4's ring, PD = 1).
+  // The loads past the span's end are not skipped: the tap iterators stop at the last
+  // tap, which is re-read (unconditional loads).  A skipped load compiles to "reg = 0;
+  // branch over the load", and that zeroing waits for the previous iteration's load
+  // into the same register (measured: 42% of the warp samples on it).
+  auto rec_ptr = [&](const TapIter& i) { return rbase + i.c * cstride + i.kh * Wp + i.kw; };
+  auto tblock = [&](const TapIter& i) { return tbase + ((int64_t)i.c * kk + i.kh * a.kw + i.kw) * tstride; };
+  TapIter tt = at(t0);  // tap of the next table entry to load, min(t + 1, t1 - 1)
+  TabTap<F> q;
+  q.load(__ldg(rec_ptr(tt)), tblock(tt), a);
+  if (t0 + 1 < t1) tt.next(a.kh, a.kw);
+  TapIter tr = tt;      // tap of the next record to load, min(t + 2, t1 - 1)
+  uint32_t rn = __ldg(rec_ptr(tr));
+  if (t0 + 2 < t1) tr.next(a.kh, a.kw);
+#pragma unroll 1
+  for (int t = t0; t < t1; t++) {
+    TabTap<F> cur = q;
+    q.load(rn, tblock(tt), a);
+    if (t + 2 < t1) tt.next(a.kh, a.kw);
+    rn = __ldg(rec_ptr(tr));
+    if (t + 3 < t1) tr.next(a.kh, a.kw);
+    F::mac_tab(acc, cur.T, cur.EA, cur.SX);
+  }
+}
+
+constexpr uint32_t SPLIT_TOKEN = 0xA5A50000u;
+
+template <class F, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) conv_tab_split_kernel(ConvArgs a) {
+  static_assert(F::NOUT <= 31, "the hand-off slot holds NOUT planes and a token in 32 words");
+  const int G = (a.cout + 31) >> 5;
+  const int64_t npix = (int64_t)a.n * a.ho * a.wo;
+  const int W = (int)gridDim.x, E = a.split_e, S = a.split_s, L = a.split_l;
+  const int taps = a.cin * a.kh * a.kw;
+  const int b = (int)blockIdx.x;
+  const int Hp = a.h + 2 * a.pad, Wp = a.w + 2 * a.pad;
+  const int64_t tstride = (int64_t)F::TAB_ROWS * tab_stride(F::NPT, F::WF);
+  struct Unit {
+    int64_t pix;
+    int g;
+    bool valid;
+    const uint32_t* rbase;
+    const uint32_t* tbase;
+    uint32_t* slot;
+  };
+  auto unit = [&](int u) {
+    Unit r;
+    r.g = u % G;
+    r.pix = (int64_t)(u / G) * NT + threadIdx.x;
+    r.valid = r.pix < npix;
+    const int64_t p = r.valid ? r.pix : 0;
+    const int ox = (int)(p % a.wo), oy = (int)((p / a.wo) % a.ho), ni = (int)(p / ((int64_t)a.wo * a.ho));
+    r.rbase = a.x + ((int64_t)ni * a.cin * Hp + (int64_t)oy * a.stride) * Wp + (int64_t)ox * a.stride;
+    r.tbase = a.wt + (int64_t)r.g * a.cin * a.kh * a.kw * tstride;
+    r.slot = a.y + p * a.cout + 32 * r.g;  // float32 output words of (pixel, group): 32 x 4 bytes
+    return r;
+  };
+  auto finish = [&](uint32_t (&acc)[F::NOUT], const Unit& u) {
+    F::canon(acc, acc);  // the chain keeps a relaxed accumulator (fpgen.build_mac_tab)
+    if (a.relu) F::relu(acc, acc);
+    if constexpr (F::WE <= 7) store_f32<F>(acc, a, u.pix, u.g);
+  };
+  // phases: 0 = own taps [0, x0) then the accumulator parked in the own output slot;
+  // 1 = segment s of the extra unit, taps [x0, x1); 2 = own taps [x0, taps).  One loop,
+  // so the circuit is emitted once and nothing but the accumulator lives across phases.
+  // a worker takes segments of extra units of its own Cout group only (the
+  // table rows it gathers are the ones its SM's other CTAs keep in L1): of group
+  // g's workers (b = g + G r), rank r takes segment r / c of the group's extra
+  // unit number r % c (c extra units in group g: W + i0 + G k, k < c)
+  const int g = b % G, r = b / G;
+  const int i0 = ((g - W) % G + G) % G;
+  const int c = i0 < E ? (E - i0 + G - 1) / G : 0;
+  const bool has_x = r < c * S;
+  const int s = has_x ? r / c : 0;
+  const int xu = has_x ? W + i0 + G * (r % c) : 0;
+  const int x0 = has_x ? s * L : 0, x1 = s == S - 1 ? taps : x0 + L;
+  // Phases, one loop (the circuit is emitted once; only the accumulator lives across
+  // phases): 0 = own taps [0, x0), then -- while segment s - 1 has not handed its
+  // accumulator on -- further own taps a kernel window (kh x kw) at a time, so no
+  // worker idles on a spin, then the own accumulator parked in the own output slot
+  // (tm taps done); 1 = segment s of the extra unit, taps [x0, x1); 2 = own taps
+  // [tm, taps).  Every lane computes (a lane past the last pixel on pixel 0) so
+  // the warp-wide ready vote sees all 32; stores and waits are per valid lane.
+  const int chunk = a.kh * a.kw;
+  const uint32_t want = SPLIT_TOKEN | (uint32_t)s;
+  uint32_t acc[F::NOUT];
+#pragma unroll
+  for (int j = 0; j < F::NOUT; j++) acc[j] = 0u;  // +0 (L9)
+  int ph = has_x ? 0 : 2, tm = 0;
+#pragma unroll 1
+  while (true) {
+    int t0, t1;
+    if (ph == 0) {
+      if (tm >= x0) {
+        bool ready = s == 0 || tm >= taps;
+        if (!ready) {
+          const Unit ex = unit(xu);
+          uint32_t v = want;
+          if (ex.valid) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ex.slot + 31) : "memory");
+          ready = __all_sync(0xffffffffu, v == want);
+        }
+        if (ready) {
+          const Unit me = unit(b);
+          if (me.valid && tm > 0) {
+#pragma unroll
+            for (int j = 0; j < F::NOUT; j++) me.slot[j] = acc[j];
+          }
+          ph = 1;
+          continue;
+        }
+        t0 = tm;
+        t1 = min(tm + chunk, taps);
+      } else {
+        t0 = 0;
+        t1 = x0;
+      }
+    } else if (ph == 1) {
+      const Unit ex = unit(xu);
+      if (s > 0 && ex.valid) {  // (only when the own taps ran out first) wait for the hand-off
+        uint32_t v, ns = 64;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ex.slot + 31) : "memory");
+          if (v == want) break;
+          __nanosleep(ns);
+          ns = min(2 * ns, 4096u);
+        }
+#pragma unroll
+        for (int j = 0; j < F::NOUT; j++) acc[j] = __ldcg(ex.slot + j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < F::NOUT; j++) acc[j] = 0u;
+      }
+      t0 = x0;
+      t1 = x1;
+    } else {
+      const Unit me = unit(b);
+#pragma unroll
+      for (int j = 0; j < F::NOUT; j++) acc[j] = tm > 0 && me.valid ? me.slot[j] : 0u;
+      t0 = tm;
+      t1 = taps;
+    }
+    const Unit u = unit(ph == 1 ? xu : b);
+    tab_span<F>(acc, a, u.rbase, u.tbase, t0, t1);
+    if (ph == 0) {
+      tm = t1;
+    } else if (ph == 1) {
+      if (u.valid) {
+        if (s < S - 1) {
+#pragma unroll
+          for (int j = 0; j < F::NOUT; j++) __stcg(u.slot + j, acc[j]);
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(u.slot + 31),
+                       "r"(SPLIT_TOKEN | (uint32_t)(s + 1))
+                       : "memory");
+        } else {
+          finish(acc, u);
+        }
+      }
+      ph = 2;
+    } else {
+      if (u.valid) finish(acc, u);
+      break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // conv2d_prepared with the weight tables staged in shared memory.
 //
 // The per-thread table-row gathers are the part of the inner loop that costs
@@ -860,10 +1064,45 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     return run(a, conv_tab_kernel<F, 128, 8, true, 0, 3>, grid(128), 128, 0, s, 6);
   } else if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
     return run(a, conv_tab_kernel<F, 32, 1, false, 3>, grid(32), 32, 0, s, 5);
-  } else if (variant == 4) {  // software-pipelined (large tables / latency-bound configs)
+  } else if (variant == 4 || variant == 12) {  // software-pipelined (large tables / latency-bound configs)
+    constexpr int M4 = F::G_TAB > 400 ? 4 : 5;
+    if constexpr (F::NOUT <= 31 && F::WE <= 7) {
+      if (variant == 12 || a.variant == 0) {
+      // variant 12 (the default for variant 4's launches with the float32 epilogue when
+      // the units overhang one wave): the fractional-wave schedule, conv_tab_split_kernel
+      if (a.out_mode == 3 && (a.cout & 31) == 0) {
+        auto kern = conv_tab_split_kernel<F, 128, M4>;
+        int dev = 0, sms = 0, nb = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, 0) != cudaSuccess)
+          return cudaGetLastError();
+        const int64_t W = (int64_t)nb * sms, U = (npix + 127) / 128 * gy, E = U - W;
+        const int taps = a.cin * a.kh * a.kw;
+        // segments per extra unit: every group's workers cover its extra units S times
+        int64_t S = E > 0 ? 16 : 0;
+        for (int64_t g = 0; g < gy && E > 0; g++) {
+          const int64_t i0 = ((g - W) % gy + gy) % gy, c = i0 < E ? (E - i0 + gy - 1) / gy : 0;
+          if (c > 0) S = std::min<int64_t>(S, ((W - g + gy - 1) / gy) / c);
+        }
+        if (E > 0 && S >= 2 && taps >= S) {
+          if (a.info) return run(a, kern, dim3((unsigned)W), 128, 0, s, 12);
+          ConvArgs b = a;
+          b.split_e = (int)E;
+          b.split_s = (int)S;
+          b.split_l = (int)(taps / S);
+          // zero the extra units' output slots (the hand-off tokens start cleared)
+          const int64_t p0 = W / gy * 128;
+          cudaError_t err = cudaMemsetAsync(b.y + p0 * a.cout, 0, (size_t)((npix - p0) * a.cout) * 4, s);
+          if (err != cudaSuccess) return err;
+          void* args[] = {&b};
+          return cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)W), dim3(128), args, 0, s);
+        }
+      }
+      }
+    }
     // <= 96 registers, 5 CTAs / SM (C3 e5m10 0.79 -> 0.81, C5 wF = 10 +0-3% vs 128 registers);
     // the extended class's largest circuits (> 400 lop3) get 128 (4 CTAs / SM)
-    constexpr int M4 = F::G_TAB > 400 ? 4 : 5;
     return run(a, conv_tab_kernel<F, 128, M4, false, 1>, grid(128), 128, 0, s, 4);
   } else if (k3) {     // kernel width 3 unrolled, <= 56 registers (9 CTAs / SM)
     return run(a, conv_tab_kernel<F, 128, 9, true, 0>, grid(128), 128, 0, s, 3);

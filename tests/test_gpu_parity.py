@@ -692,7 +692,7 @@ def test_f32_epilogue_matches_oracle_decode(we, wf, ext, cout):
             if H.wtab_words(f, 3, 3, cin, cout) > 0:
                 tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
                 xr = H.quantize_activations(f, torch.from_numpy(x).cuda(), 1)
-                for variant in (0, 4, 5, 6, 7, 8):
+                for variant in (0, 4, 5, 6, 7, 8, 12):
                     got = _f32_bits(H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, relu,
                                                       variant=variant, nxt=H.F32))
                     assert np.array_equal(got, exp), ("tables", variant, rnd, relu)
@@ -810,3 +810,40 @@ def test_chain_public_api_vs_oracle(we, wfs, exts, rnd):
     exp = oracle.decode_f64(exp_w, we, wfo).astype(np.float32)
     assert y.shape == exp.shape
     assert np.array_equal(y.view(np.uint32), exp.view(np.uint32))
+
+
+@pytest.mark.parametrize("we,wf,rnd,relu", [(5, 10, 0, 0), (5, 10, 1, 1), (6, 9, 0, 1), (4, 10, 0, 1)])
+def test_fractional_wave_schedule(we, wf, rnd, relu):
+    """Variant 12 (C5-like layer with a ragged last tile: 61 images of 14 x 14 -> 94
+    tiles x 8 Cout groups = 752 units on 740 resident CTAs): every float32 output
+    equals variant 4's (one thread per chain) and the automatic schedule's, and a
+    sample -- most of it in the
+    units whose chains were handed between CTAs (the last 12) -- equals the
+    oracle's chains decoded."""
+    H = hobf()
+    n, h, w, cin, cout = 61, 14, 14, 32, 256
+    x, wt = inputs.small_case(1200 + wf, n, h, w, cin, cout, "uniform4", 0.05)
+    f = H.Fmt(we, wf, rnd)
+    info = H.conv_kernel_info(H.OP_PREPARED, f, n, h, w, cin, 3, 3, cout, 1, 1, nxt=H.F32, variant=12)
+    ctas = info["ctas_per_sm"] * torch.cuda.get_device_properties(0).multi_processor_count
+    units = (n * h * w + 127) // 128 * (cout // 32)
+    assert ctas < units <= ctas + ctas // 2 and info["variant"] == 12 and info["blocks"] == ctas, (info, units)
+    wp = H.quantize_pack(we, wf, torch.from_numpy(wt.reshape(-1, cout)).cuda(), rnd)
+    tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
+    xr = H.quantize_activations(f, torch.from_numpy(x).cuda(), 1)
+    y = {}
+    for v in (0, 4, 12):
+        out = torch.full((n * h * w, cout), float("nan"), device="cuda")  # stale contents must not matter
+        y[v] = _f32_bits(H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, relu, out=out,
+                                           variant=v, nxt=H.F32))
+    assert np.array_equal(y[0], y[4]) and np.array_equal(y[12], y[4])
+    rng = np.random.default_rng(wf)
+    npix = n * h * w
+    last = (units - 12) // (cout // 32) * 128  # first pixel of the handed-off units (740 resident CTAs)
+    pix = np.concatenate([rng.integers(last, npix, 600), rng.integers(0, npix, 200)])
+    idx = pix * cout + rng.integers(0, cout, pix.size)
+    xq = oracle.encode_f32(x, we, wf, rnd)
+    wq = oracle.encode_f32(wt, we, wf, rnd)
+    exp_w = oracle.conv2d_sample(xq, wq, idx, we, wf, wf + 1, rnd, relu=relu)
+    exp = oracle.decode_f64(exp_w, we, wf + 1).astype(np.float32).view(np.uint32)
+    assert np.array_equal(y[0].ravel()[idx], exp)

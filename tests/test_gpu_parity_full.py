@@ -113,9 +113,14 @@ def test_C5_whole_images_every_format(we, wf):
     for rnd, imgs in ((0, (0, cfg.n - 1)), (1, (0, cfg.n - 1))):
         f = H.Fmt(we, wf, rnd)
         got = gpu_bench_path(x, w, f, cfg)
+        # the float32 epilogue the bench times (for wF = 10 and e6m9 the fractional-wave
+        # schedule, variant 12: the last image's chains are handed between CTAs)
+        y32 = gpu_bench_path(x, w, f, cfg, f32=True)
         for i in imgs:
             exp = oracle_words(x[i:i + 1], w, f, cfg)[0]
             assert np.array_equal(got[i], exp), ((we, wf, rnd, i), first_mismatches(got[i], exp))
+            dec = oracle.decode_f64(exp, we, f.wfo).astype(np.float32)
+            assert np.array_equal(y32[i].view(np.uint32), dec.view(np.uint32)), ("f32", we, wf, rnd, i)
 
 
 _C5 = {}

@@ -23,6 +23,7 @@ ap.add_argument("--kernel", default="tables")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--round", type=int, default=0)
 ap.add_argument("--variant", type=int, default=0, help="hobf_conv2d_prepared_ex schedule (0 = automatic)")
+ap.add_argument("--f32", action="store_true", help="float32 epilogue (the bench's output; variant 12 needs it)")
 ap.add_argument("--n", type=int, default=0, help="batch override (a rank's share under the strong split)")
 a = ap.parse_args()
 cfg = inputs.CONFIGS[a.config]
@@ -39,7 +40,7 @@ if a.kernel == "tables":
     wt = H.prepare_weights(f, wp, 3, 3, cfg.cin, cfg.cout)
     xr = H.prepare_activations(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, cfg.pad)
     run = lambda: H.conv2d_prepared(f, xr, cfg.n, cfg.h, cfg.w, cfg.cin, wt, 3, 3, cfg.cout,  # noqa: E731
-                                    cfg.stride, cfg.pad, variant=a.variant)
+                                    cfg.stride, cfg.pad, variant=a.variant, nxt=H.F32 if a.f32 else None)
     G = g["mac_tab"]
 else:
     run = lambda: H.conv2d(f, xp, cfg.n, cfg.h, cfg.w, cfg.cin, wp, 3, 3, cfg.cout, cfg.stride, cfg.pad)  # noqa: E731
@@ -60,6 +61,6 @@ ms = float(np.median(ts))
 macs = cfg.macs()
 peak = 148 * 64 * 1.965e9
 print(json.dumps({"config": a.config, "n": cfg.n, "format": f"e{we}m{wf}", "kernel": a.kernel,
-                  "variant": a.variant, "ms": ms,
+                  "variant": a.variant, "f32": a.f32, "ms": ms,
                   "mac_per_s": macs / ms * 1e3, "G": G, "frac": macs * G / 32 / (ms * 1e-3) / peak,
                   "same_as_first": bool(torch.equal(y, y0))}))
