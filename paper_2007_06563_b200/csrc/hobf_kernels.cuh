@@ -1096,7 +1096,14 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
           cudaError_t err = cudaMemsetAsync(b.y + p0 * a.cout, 0, (size_t)((npix - p0) * a.cout) * 4, s);
           if (err != cudaSuccess) return err;
           void* args[] = {&b};
-          return cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)W), dim3(128), args, 0, s);
+          err = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)W), dim3(128), args, 0, s);
+          // a device / context that cannot co-schedule the W workers (MPS partition, no
+          // cooperative launch): nothing ran, fall through to variant 4 (same results)
+          if (err != cudaErrorCooperativeLaunchTooLarge && err != cudaErrorNotSupported &&
+              err != cudaErrorNotPermitted)
+            return err;
+          (void)cudaGetLastError();
+          if (a.variant == 12) return err;  // forced by the caller: report it
         }
       }
       }
