@@ -243,7 +243,10 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
  * past the wave, the segment accumulators handed on through the units' own
  * float32 output slots (zeroed first, one cudaMemsetAsync) -- the automatic
  * choice where variant 4 would be; otherwise it runs as variant 4.  Variant 12
- * launches the conv through cudaLaunchCooperativeKernel.
+ * launches the conv through cudaLaunchCooperativeKernel (a device or context
+ * that cannot co-schedule the workers: variant 4 runs instead, unless 12 / 13
+ * was asked for explicitly, which returns HOBF_ECUDA); 13 = variant 12 at 4
+ * CTAs per SM (128 registers).
  * Variants 3 and 6 need kw == 3 (others fall back to the generic loop).  Every
  * variant
  * runs the same circuit over the same serial (c, kh, kw) order: identical

@@ -981,6 +981,51 @@ inline int64_t busiest_2per(int64_t npix, int64_t gy, int nt) {
 inline int64_t busiest352(int64_t npix, int64_t gy) { return busiest_2per(npix, gy, 352); }
 inline int64_t busiest256(int64_t npix, int64_t gy) { return busiest_2per(npix, gy, 256); }
 
+// Fractional-wave launch (conv_tab_split_kernel at MB CTAs per SM).  done = false: the
+// shape does not call for it (no overhang, too few workers per extra unit) or the
+// device cannot co-schedule the workers -- nothing ran, the caller launches variant 4.
+template <class F, int MB>
+cudaError_t launch_split(const ConvArgs& a, cudaStream_t s, int64_t npix, unsigned gy, bool& done) {
+  done = false;
+  auto kern = conv_tab_split_kernel<F, 128, MB>;
+  int dev = 0, sms = 0, nb = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, 0) != cudaSuccess) {
+    done = true;
+    return cudaGetLastError();
+  }
+  const int64_t W = (int64_t)nb * sms, U = (npix + 127) / 128 * gy, E = U - W;
+  const int taps = a.cin * a.kh * a.kw;
+  // segments per extra unit: every group's workers cover its extra units S times
+  int64_t S = E > 0 ? 16 : 0;
+  for (int64_t g = 0; g < gy && E > 0; g++) {
+    const int64_t i0 = ((g - W) % gy + gy) % gy, c = i0 < E ? (E - i0 + gy - 1) / gy : 0;
+    if (c > 0) S = std::min<int64_t>(S, ((W - g + gy - 1) / gy) / c);
+  }
+  if (!(E > 0 && S >= 2 && taps >= S)) return cudaSuccess;
+  done = true;
+  if (a.info) return run(a, kern, dim3((unsigned)W), 128, 0, s, MB == 4 && a.variant != 12 ? 13 : 12);
+  ConvArgs b = a;
+  b.split_e = (int)E;
+  b.split_s = (int)S;
+  b.split_l = (int)(taps / S);
+  // zero the extra units' output slots (the hand-off tokens start cleared)
+  const int64_t p0 = W / gy * 128;
+  cudaError_t err = cudaMemsetAsync(b.y + p0 * a.cout, 0, (size_t)((npix - p0) * a.cout) * 4, s);
+  if (err != cudaSuccess) return err;
+  void* args[] = {&b};
+  err = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)W), dim3(128), args, 0, s);
+  // a device / context that cannot co-schedule the W workers (MPS partition, no
+  // cooperative launch): nothing ran, fall back to variant 4 (same results)
+  if (err != cudaErrorCooperativeLaunchTooLarge && err != cudaErrorNotSupported && err != cudaErrorNotPermitted)
+    return err;
+  (void)cudaGetLastError();
+  if (a.variant == 12 || a.variant == 13) return err;  // forced by the caller: report it
+  done = false;
+  return cudaSuccess;
+}
+
 template <class F>
 cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
   const int64_t npix = (int64_t)a.n * a.ho * a.wo;
@@ -1064,48 +1109,22 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     return run(a, conv_tab_kernel<F, 128, 8, true, 0, 3>, grid(128), 128, 0, s, 6);
   } else if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
     return run(a, conv_tab_kernel<F, 32, 1, false, 3>, grid(32), 32, 0, s, 5);
-  } else if (variant == 4 || variant == 12) {  // software-pipelined (large tables / latency-bound configs)
+  } else if (variant == 4 || variant == 12 || variant == 13) {  // software-pipelined (large tables / latency-bound configs)
     constexpr int M4 = F::G_TAB > 400 ? 4 : 5;
     if constexpr (F::NOUT <= 31 && F::WE <= 7) {
-      if (variant == 12 || a.variant == 0) {
-      // variant 12 (the default for variant 4's launches with the float32 epilogue when
-      // the units overhang one wave): the fractional-wave schedule, conv_tab_split_kernel
-      if (a.out_mode == 3 && (a.cout & 31) == 0) {
-        auto kern = conv_tab_split_kernel<F, 128, M4>;
-        int dev = 0, sms = 0, nb = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 128, 0) != cudaSuccess)
-          return cudaGetLastError();
-        const int64_t W = (int64_t)nb * sms, U = (npix + 127) / 128 * gy, E = U - W;
-        const int taps = a.cin * a.kh * a.kw;
-        // segments per extra unit: every group's workers cover its extra units S times
-        int64_t S = E > 0 ? 16 : 0;
-        for (int64_t g = 0; g < gy && E > 0; g++) {
-          const int64_t i0 = ((g - W) % gy + gy) % gy, c = i0 < E ? (E - i0 + gy - 1) / gy : 0;
-          if (c > 0) S = std::min<int64_t>(S, ((W - g + gy - 1) / gy) / c);
-        }
-        if (E > 0 && S >= 2 && taps >= S) {
-          if (a.info) return run(a, kern, dim3((unsigned)W), 128, 0, s, 12);
-          ConvArgs b = a;
-          b.split_e = (int)E;
-          b.split_s = (int)S;
-          b.split_l = (int)(taps / S);
-          // zero the extra units' output slots (the hand-off tokens start cleared)
-          const int64_t p0 = W / gy * 128;
-          cudaError_t err = cudaMemsetAsync(b.y + p0 * a.cout, 0, (size_t)((npix - p0) * a.cout) * 4, s);
-          if (err != cudaSuccess) return err;
-          void* args[] = {&b};
-          err = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)W), dim3(128), args, 0, s);
-          // a device / context that cannot co-schedule the W workers (MPS partition, no
-          // cooperative launch): nothing ran, fall through to variant 4 (same results)
-          if (err != cudaErrorCooperativeLaunchTooLarge && err != cudaErrorNotSupported &&
-              err != cudaErrorNotPermitted)
-            return err;
-          (void)cudaGetLastError();
-          if (a.variant == 12) return err;  // forced by the caller: report it
-        }
-      }
+      // variants 12 / 13 (the default for variant 4's launches with the float32 epilogue
+      // when the units overhang one wave): the fractional-wave schedule,
+      // conv_tab_split_kernel, at M4 (12) or 4 (13) CTAs / SM.  Automatic: 4 CTAs / SM
+      // (128 registers) from NOUT = 19, where the 96-register kernel spills inside the
+      // tap loop (C5 e6m10 0.63 -> 0.69, e5m10 0.67 -> 0.69, e6m9 0.66 -> 0.69 of the
+      // roof; e4m10, NOUT = 18, no spills: 0.64 at 5 vs 0.625 at 4;
+      // profiles/r02_c5_split13.txt)
+      if ((variant == 12 || variant == 13 || a.variant == 0) && a.out_mode == 3 && (a.cout & 31) == 0) {
+        bool done = false;
+        const bool four = variant == 13 || (a.variant == 0 && F::NOUT >= 19);
+        const cudaError_t err = four ? launch_split<F, 4>(a, s, npix, gy, done)
+                                     : launch_split<F, M4>(a, s, npix, gy, done);
+        if (done) return err;
       }
     }
     // <= 96 registers, 5 CTAs / SM (C3 e5m10 0.79 -> 0.81, C5 wF = 10 +0-3% vs 128 registers);
