@@ -1059,6 +1059,17 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     variant = (smem_ok && warps >= 148) ? 7
               : warps < 148 * 4 * 2 ? 5 : smem_ok ? 7 : units_ok ? 8 : (F::WF >= 6 ? 4 : (k3 ? 6 : 3));
   }
+  if constexpr (F::WF == 9 && F::NOUT >= 19 && F::NOUT <= 31 && F::WE <= 7) {
+    // e6m9: its tap-staged kernel holds 2 CTAs / SM and measured 0.66 / 0.65 of the roof
+    // (RNE / RTZ) on C5, the L1-served fractional wave at 4 CTAs / SM 0.69 / 0.68
+    // (profiles/r02_c5_split13_wf89.txt; e4m9 / e5m9, NOUT = 17 / 18: staged 0.75 vs 0.62)
+    if (a.variant == 0 && variant == 8 && ut == 1 && 6 * tap_bytes > 216 * 1024 && a.out_mode == 3 &&
+        (a.cout & 31) == 0) {
+      bool done = false;
+      const cudaError_t err = launch_split<F, 4>(a, s, npix, gy, done);
+      if (done) return err;
+    }
+  }
   int shape = 0;  // variants 10 / 11: variant 7 with the CTA shape forced (256 x 3 / 128 x 6)
   if (variant >= 10 && variant <= 11) {
     shape = variant;
@@ -1121,7 +1132,18 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
       // profiles/r02_c5_split13.txt)
       if ((variant == 12 || variant == 13 || a.variant == 0) && a.out_mode == 3 && (a.cout & 31) == 0) {
         bool done = false;
-        const bool four = variant == 13 || (a.variant == 0 && F::NOUT >= 19);
+        bool four = variant == 13 || (a.variant == 0 && F::NOUT >= 19);
+        if (four && a.variant == 0 && M4 > 4) {
+          // units that fit one wave of variant 4's own M4 CTAs / SM run there (C5 e5m10 at
+          // 60 images, 736 units on 740 slots: 0.73 of the roof vs 0.65 split over 592)
+          int dev = 0, sms = 0, nb = 0;
+          if (cudaGetDevice(&dev) == cudaSuccess &&
+              cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, conv_tab_kernel<F, 128, M4, false, 1>, 128, 0) ==
+                  cudaSuccess &&
+              (int64_t)(npix + 127) / 128 * gy <= (int64_t)nb * sms)
+            four = false;  // (launch_split then finds no overhang and variant 4 runs)
+        }
         const cudaError_t err = four ? launch_split<F, 4>(a, s, npix, gy, done)
                                      : launch_split<F, M4>(a, s, npix, gy, done);
         if (done) return err;
