@@ -246,7 +246,15 @@ hobf_status hobf_conv2d_dw(hobf_fmt f, const uint32_t* d_x_planes, int32_t n, in
  * launches the conv through cudaLaunchCooperativeKernel (a device or context
  * that cannot co-schedule the workers: variant 4 runs instead, unless 12 / 13
  * was asked for explicitly, which returns HOBF_ECUDA); 13 = variant 12 at 4
- * CTAs per SM (128 registers).
+ * CTAs per SM (128 registers); 14 = variant 4 with a progress throttle (the
+ * float32 epilogue, cout % 32 == 0, else it runs as variant 4): every CTA
+ * publishes the number of input channels it has finished as a token in one of
+ * its own output words, and a warp more than two channels ahead of the slowest
+ * of 32 CTAs of its Cout group sleeps (bounded) -- an experiment in keeping a
+ * group's table gathers inside the L2 window; never the automatic choice;
+ * 15 = variant 4 with warp-cooperative table gathers: 8 lanes copy the 16-byte
+ * chunks of one table row (cp.async, 4 rows per instruction) into a per-warp
+ * shared-memory slot a tap ahead, and each thread reads its own row back.
  * Variants 3 and 6 need kw == 3 (others fall back to the generic loop).  Every
  * variant
  * runs the same circuit over the same serial (c, kh, kw) order: identical

@@ -1087,7 +1087,7 @@ static hobf_status conv_setup(int op, hobf_fmt f, const uint32_t* x, int32_t n, 
                               int32_t relu, hobf_epilogue ep, void* out, int32_t variant, bool launch, ConvArgs& a,
                               const FormatEntry*& e, bool* empty) {
   *empty = false;
-  if (op == OP_PREPARED ? (variant != 0 && (variant < 3 || variant > 13 || variant == 9)) : variant != 0)
+  if (op == OP_PREPARED ? (variant != 0 && (variant < 3 || variant > 15 || variant == 9)) : variant != 0)
     return HOBF_EINVAL;
   if (!fmt_ok(f.we, f.wf) || (f.round != 0 && f.round != 1) || (f.extended != 0 && f.extended != 1))
     return HOBF_EINVAL;

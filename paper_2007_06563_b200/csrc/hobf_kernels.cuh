@@ -364,14 +364,36 @@ struct TabTap {
 // unrolled loop body.  PD > 0: software pipeline -- the table entries of taps
 // t+1..t+PD and the record of tap t+PD+1 are in flight while the MAC of tap t
 // runs (latency-bound configs, large tables).
-template <class F, int NT, int MINB, bool KW3, int PD, int RU = 1>
+// THR (variant 14, the float32 epilogue): a progress throttle.  The CTAs of a Cout
+// group gather from the same table blocks; left alone they spread over more taps
+// than L2 holds (profiles/r02_c5_e5m10_one_wave.txt).  Here thread 0 of a CTA
+// publishes the number of input channels it has finished (a token in its own
+// float32 output word, overwritten by the output at the end), and each warp, once
+// per input channel, reads the tokens of 32 CTAs of its group and sleeps (bounded:
+// 16 x 250 ns) while it is more than THR_D channels ahead of the slowest of them.
+// Waits are bounded and words that are not tokens (CTAs not started, finished) are
+// ignored, so the schedule cannot deadlock and the results do not depend on it.
+constexpr uint32_t THR_TOKEN = 0xA5A50000u;
+constexpr int THR_D = 2;
+
+// COOP (variant 15): warp-cooperative table gathers.  A warp's 32 row gathers
+// cost the L1 tag stage 32 lines per 128-bit load instruction (6 instructions per
+// tap at wF = 9, 10).  Here 8 lanes copy the 16-byte chunks of one row (4 rows per
+// instruction: ~4-8 lines) with cp.async into a per-warp shared-memory slot, a tap
+// ahead, double-buffered; each thread then reads its own row back with 128-bit
+// shared loads (row stride NPT + 4 words: conflict-free quads).  No table registers
+// are held across the MAC.  Every lane computes (a lane past the last pixel on
+// pixel 0) so that the warp-wide shuffles and barriers see all 32 lanes.
+template <class F, int NT, int MINB, bool KW3, int PD, int RU = 1, bool THR = false, bool COOP = false>
 __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   // linear grid, output-channel group fastest: the G groups of a pixel tile run
   // together, so each activation record comes from DRAM once and is reused from L2
   const int G = (a.cout + 31) >> 5;
   const int g = (int)(blockIdx.x % G);
-  const int64_t pix = (int64_t)(blockIdx.x / G) * blockDim.x + threadIdx.x;
-  if (pix >= (int64_t)a.n * a.ho * a.wo) return;
+  const int64_t pix_t = (int64_t)(blockIdx.x / G) * blockDim.x + threadIdx.x;
+  const bool valid = pix_t < (int64_t)a.n * a.ho * a.wo;
+  if (!COOP && !valid) return;
+  const int64_t pix = valid ? pix_t : 0;
   const int ox = (int)(pix % a.wo);
   const int oy = (int)((pix / a.wo) % a.ho);
   const int ni = (int)(pix / ((int64_t)a.wo * a.ho));
@@ -392,7 +414,57 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
   auto rec_at = [&](int c, int kh, int kw) { return __ldg(rbase + c * cstride + kh * Wp + kw); };
   auto tblock = [&](int c, int kh, int kw) { return tbase + ((int64_t)c * a.kh * KW + kh * KW + kw) * tstride; };
 
-  if constexpr (PD == 0 && KW3) {
+  if constexpr (COOP) {
+    constexpr int CH = F::NPT / 4, RS = F::NPT + 4;  // 16-byte chunks per row; padded slot row (words)
+    static_assert(CH <= 8 && F::NPT % 4 == 0, "8 lanes copy one row");
+    __shared__ __align__(16) uint32_t cbuf[NT / 32][2][32][RS];
+    const int lane = (int)(threadIdx.x & 31), wrp = (int)(threadIdx.x >> 5);
+    const int sub = lane >> 3, m = lane & 7;
+    constexpr int rstride = tab_stride(F::NPT, F::WF);
+    auto issue = [&](uint32_t rec, const uint32_t* __restrict__ tb, int b) {
+      const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const int sl = 4 * q + sub;  // the lane whose row this lane helps to copy
+        const uint32_t r = __shfl_sync(0xffffffffu, row, sl);
+        if (m < CH) {
+          const uint32_t* src = tb + (int64_t)r * rstride + 4 * m;
+          const uint32_t dst = smem_addr(&cbuf[wrp][b][sl][4 * m]);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int taps = a.cin * a.kh * KW;
+    TapIter tt, tr;  // tap of the next table rows to copy (t + 1) / of the next record to load (t + 2)
+    uint32_t rc = rec_at(0, 0, 0);
+    issue(rc, tblock(0, 0, 0), 0);
+    tt.next(a.kh, KW);
+    uint32_t rn = tt.c < a.cin ? rec_at(tt.c, tt.kh, tt.kw) : 0u;
+    tr = tt;
+    tr.next(a.kh, KW);
+#pragma unroll 1
+    for (int t = 0; t < taps; t++) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      uint32_t T[F::NPT], EA[F::WE], SX[1];
+      const uint4* p4 = reinterpret_cast<const uint4*>(&cbuf[wrp][t & 1][lane][0]);
+#pragma unroll
+      for (int q = 0; q < CH; q++) {
+        const uint4 v = p4[q];
+        T[4 * q + 0] = v.x; T[4 * q + 1] = v.y; T[4 * q + 2] = v.z; T[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int j = 0; j < F::WE; j++) EA[j] = (uint32_t)__mulhi((int32_t)(rc * a.lift[F::WF + j]), a.one);
+      SX[0] = (uint32_t)__mulhi((int32_t)(rc * a.lift[F::WF + F::WE]), a.one);
+      if (tt.c < a.cin) issue(rn, tblock(tt.c, tt.kh, tt.kw), (t + 1) & 1);
+      tt.next(a.kh, KW);
+      rc = rn;
+      rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
+      tr.next(a.kh, KW);
+      F::mac_tab(acc, T, EA, SX);
+    }
+  } else if constexpr (PD == 0 && KW3) {
     // the 3 records of the next kernel row are loaded while this row's 3 MACs run
     uint32_t rn[3];
 #pragma unroll
@@ -483,6 +555,7 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
       tr = tt;
       uint32_t rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
       tr.next(a.kh, KW);
+      [[maybe_unused]] int left = a.kh * KW, cdone = 0;
 #pragma unroll 1
       for (int t = 0; t < taps; t++) {
         TabTap<F> cur = q[0];
@@ -493,12 +566,30 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
         rn = tr.c < a.cin ? rec_at(tr.c, tr.kh, tr.kw) : 0u;
         tr.next(a.kh, KW);
         F::mac_tab(acc, cur.T, cur.EA, cur.SX);
+        if constexpr (THR) {
+          if (--left == 0) {  // an input channel done
+            left = a.kh * KW;
+            ++cdone;
+            const int tile = (int)(blockIdx.x / G), ntiles = (int)(gridDim.x / G);
+            volatile uint32_t* slots = a.y + 32 * g + 31;  // word 31 of (pixel, group g)'s 32 floats
+            if (threadIdx.x == 0) slots[(int64_t)tile * NT * a.cout] = THR_TOKEN | (uint32_t)cdone;
+            const unsigned m = __activemask();
+            const int lane = (int)(threadIdx.x & 31);
+            const int peer = (tile + 1 + lane * max(1, ntiles / 32)) % ntiles;
+            for (int k = 0; k < 16; k++) {
+              const uint32_t v = slots[(int64_t)peer * NT * a.cout];
+              const int prog = (v >> 16) == (THR_TOKEN >> 16) ? (int)(v & 0xffffu) : 0x7fffffff;
+              if (cdone <= __reduce_min_sync(m, prog) + THR_D) break;
+              __nanosleep(250);
+            }
+          }
+        }
       }
     }
   }
   F::canon(acc, acc);  // the chain keeps a relaxed accumulator (fpgen.build_mac_tab)
   if (a.relu) F::relu(acc, acc);
-  store_out<F>(acc, a, pix, g, ni, oy, ox);
+  if (valid) store_out<F>(acc, a, pix, g, ni, oy, ox);
 }
 
 // ---------------------------------------------------------------------------
@@ -1120,7 +1211,7 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
     return run(a, conv_tab_kernel<F, 128, 8, true, 0, 3>, grid(128), 128, 0, s, 6);
   } else if (variant == 5) {  // latency-bound: 32-thread CTAs spread over all SMs
     return run(a, conv_tab_kernel<F, 32, 1, false, 3>, grid(32), 32, 0, s, 5);
-  } else if (variant == 4 || variant == 12 || variant == 13) {  // software-pipelined (large tables / latency-bound configs)
+  } else if (variant == 4 || (variant >= 12 && variant <= 15)) {  // software-pipelined (large tables / latency-bound configs)
     constexpr int M4 = F::G_TAB > 400 ? 4 : 5;
     if constexpr (F::NOUT <= 31 && F::WE <= 7) {
       // variants 12 / 13 (the default for variant 4's launches with the float32 epilogue
@@ -1149,6 +1240,11 @@ cudaError_t launch_conv_tab(const ConvArgs& a, cudaStream_t s) {
         if (done) return err;
       }
     }
+    if constexpr (F::NPT % 4 == 0 && F::NPT <= 32) {
+      if (variant == 15) return run(a, conv_tab_kernel<F, 128, M4, false, 1, 1, false, true>, grid(128), 128, 0, s, 15);
+    }
+    if (variant == 14 && a.out_mode == 3 && (a.cout & 31) == 0 && a.cin < 65536)
+      return run(a, conv_tab_kernel<F, 128, M4, false, 1, 1, true>, grid(128), 128, 0, s, 14);
     // <= 96 registers, 5 CTAs / SM (C3 e5m10 0.79 -> 0.81, C5 wF = 10 +0-3% vs 128 registers);
     // the extended class's largest circuits (> 400 lop3) get 128 (4 CTAs / SM)
     return run(a, conv_tab_kernel<F, 128, M4, false, 1>, grid(128), 128, 0, s, 4);

@@ -832,11 +832,14 @@ def test_fractional_wave_schedule(we, wf, rnd, relu):
     tab = H.prepare_weights(f, wp, 3, 3, cin, cout)
     xr = H.quantize_activations(f, torch.from_numpy(x).cuda(), 1)
     y = {}
-    for v in (0, 4, 12, 13):  # 13 = the fractional wave at 4 CTAs / SM (592 workers, 160 extra units)
+    # 13 = the fractional wave at 4 CTAs / SM (592 workers, 160 extra units); 14 = variant 4 with the
+    # progress throttle (tokens in the output words while the chains run)
+    # 15 = variant 4 with warp-cooperative cp.async table gathers through shared memory
+    for v in (0, 4, 12, 13, 14, 15):
         out = torch.full((n * h * w, cout), float("nan"), device="cuda")  # stale contents must not matter
         y[v] = _f32_bits(H.conv2d_prepared(f, xr, n, h, w, cin, tab, 3, 3, cout, 1, 1, relu, out=out,
                                            variant=v, nxt=H.F32))
-    assert np.array_equal(y[0], y[4]) and np.array_equal(y[12], y[4]) and np.array_equal(y[13], y[4])
+    assert all(np.array_equal(y[v], y[4]) for v in (0, 12, 13, 14, 15))
     rng = np.random.default_rng(wf)
     npix = n * h * w
     last = (units - 12) // (cout // 32) * 128  # first pixel of the handed-off units (740 resident CTAs)
