@@ -76,7 +76,7 @@ def test_argument_errors_are_synchronous_and_need_no_gpu():
         assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, ep, P, 0, None) == 1
         assert lib.hobf_conv2d_dw(f, P, 1, 4, 4, 8, P, 3, 3, 1, 1, 0, ep, P, None) == 1
     assert lib.hobf_conv2d_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(hobf.OUT_NEXT_RECORDS, 3, 1), P, None) == 1
-    assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(0, 0, 0), P, 13, None) == 1
+    assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(0, 0, 0), P, 16, None) == 1
     assert lib.hobf_conv2d_prepared_ex(f, P, 1, 4, 4, 4, P, 3, 3, 8, 1, 1, 0, E(0, 0, 0), P, 9, None) == 1
     assert lib.hobf_conv2d_dw(f, P, 1, 2, 2, 8, P, 5, 5, 1, 0, 0, E(0, 0, 0), P, None) == 2
     # beyond the launch grid's limits -> ESHAPE (not a launch failure)
@@ -93,7 +93,7 @@ def test_argument_errors_are_synchronous_and_need_no_gpu():
     info = hobf.hobf_kernel_info()
     assert lib.hobf_conv_kernel_info(3, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 0, ctypes.byref(info)) == 1
     assert lib.hobf_conv_kernel_info(1, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 0, None) == 1
-    assert lib.hobf_conv_kernel_info(1, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 13, ctypes.byref(info)) == 1
+    assert lib.hobf_conv_kernel_info(1, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 16, ctypes.byref(info)) == 1
     assert lib.hobf_conv_kernel_info(0, f, 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 4, ctypes.byref(info)) == 1
     assert lib.hobf_conv_kernel_info(1, f, 1, 2, 2, 4, 5, 5, 8, 1, 0, E(0, 0, 0), 0, ctypes.byref(info)) == 2
     assert lib.hobf_conv_kernel_info(1, hobf.Fmt(7, 3).c(), 1, 4, 4, 4, 3, 3, 8, 1, 1, E(0, 0, 0), 0,
