@@ -297,7 +297,7 @@ def test_conv_prepared_full_vs_oracle(we, wf):
             assert np.array_equal(got, gpu_conv(x, w, f, relu=relu, prepared=False))
 
 
-@pytest.mark.parametrize("variant", [3, 4, 5, 6, 7, 8, 10, 11])
+@pytest.mark.parametrize("variant", [3, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 15])  # 12-14 run as 4 here (planes out)
 @pytest.mark.parametrize("we,wf,kh,kw", [(5, 3, 3, 3), (4, 6, 2, 3), (5, 10, 3, 3), (6, 2, 3, 2), (4, 6, 3, 3),
                                          (5, 7, 3, 3), (5, 8, 3, 3), (6, 9, 3, 3)])
 def test_conv_prepared_every_schedule(variant, we, wf, kh, kw):
@@ -468,7 +468,7 @@ def test_conv_extended_class(we, wf, prepared):
         assert np.array_equal(got, exp), np.argwhere(got != exp)[:5]
 
 
-@pytest.mark.parametrize("variant", [4, 6, 7, 8, 10, 11])
+@pytest.mark.parametrize("variant", [4, 6, 7, 8, 10, 11, 15])
 @pytest.mark.parametrize("we,wf", [(5, 3), (6, 5), (4, 6), (5, 7), (5, 8), (5, 9)])
 def test_conv_extended_every_schedule(variant, we, wf):
     """Extended class through the explicit schedules (the auto schedule of the small
