@@ -419,18 +419,24 @@ __global__ void __launch_bounds__(NT, MINB) conv_tab_kernel(ConvArgs a) {
     static_assert(CH <= 8 && F::NPT % 4 == 0, "8 lanes copy one row");
     __shared__ __align__(16) uint32_t cbuf[NT / 32][2][32][RS];
     const int lane = (int)(threadIdx.x & 31), wrp = (int)(threadIdx.x >> 5);
-    const int sub = lane >> 3, m = lane & 7;
     constexpr int rstride = tab_stride(F::NPT, F::WF);
+    // lane = 8 s + m copies chunk m of the rows of lanes 8 s + q, q = 0..7: the row comes
+    // by a width-8 shuffle (source lane q of the own 8-lane segment: an immediate), the
+    // slot address is a per-thread base plus immediates, the source a 32-bit word offset
+    // (IMADs on the FMA pipe) on the tap's uniform block pointer -- no ALU-pipe work
+    const uint32_t m4 = 4u * (uint32_t)(lane & 7);
+    const bool copies = (lane & 7) < CH;
+    const uint32_t dst0 = smem_addr(&cbuf[wrp][0][lane & 24][4 * (lane & 7)]);
     auto issue = [&](uint32_t rec, const uint32_t* __restrict__ tb, int b) {
       const uint32_t row = __umulhi(rec, a.row_mul);  // rec >> 20
+      const uint32_t dstb = dst0 + (uint32_t)b * (uint32_t)(32 * RS * 4);
 #pragma unroll
       for (int q = 0; q < 8; q++) {
-        const int sl = 4 * q + sub;  // the lane whose row this lane helps to copy
-        const uint32_t r = __shfl_sync(0xffffffffu, row, sl);
-        if (m < CH) {
-          const uint32_t* src = tb + (int64_t)r * rstride + 4 * m;
-          const uint32_t dst = smem_addr(&cbuf[wrp][b][sl][4 * m]);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        const uint32_t r = __shfl_sync(0xffffffffu, row, q, 8);
+        if (copies) {
+          const uint32_t* src = tb + (r * (uint32_t)rstride + m4);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dstb + (uint32_t)(q * RS * 4)), "l"(src)
+                       : "memory");
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
